@@ -1,0 +1,140 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY. A plain, slow, obviously-correct CPU
+ * reference for what the GPU path computes. Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant with paper_1501_05387_b200/.
+ *
+ * What it computes is the PLAIN DEFINITION the method reaches exactly
+ * (DESIGN.md "Oracle"):
+ *
+ *   oracle_bfs  -- depth[v] = number of edges on a shortest src->v path that
+ *                  follows CSR out-edges, -1 if unreachable; pred[v] = the
+ *                  vertex that first discovered v in FIFO order, pred[src] =
+ *                  src (reading A-1), -1 if unreachable (A-2).
+ *                  Paper: BFS labels are "the distance from the source" and
+ *                  pred "the predecessor vertex's ID" (PAPER.md P:892-897,
+ *                  P:910-912, §5.1). Algorithm: the textbook FIFO queue BFS.
+ *
+ *   oracle_sssp -- dist[v] = min over src->v paths of the sum of the integer
+ *                  edge weights, UINT32_MAX if unreachable (A-2); weights are
+ *                  non-negative (§4.1 "We assume weights between
+ *                  nodes are all non-negative, which permits the use of
+ *                  Dijkstra's algorithm"). Algorithm: textbook Dijkstra with
+ *                  a binary heap and lazy deletion, accumulated in uint64.
+ *                  pred[v] = the vertex whose relaxation last lowered dist[v]
+ *                  (a tight parent), pred[src] = src.
+ *
+ * Return codes: 0 ok, 1 bad argument (src out of range / n <= 0),
+ * 2 out of memory, 3 a distance does not fit in uint32 (reading A-19).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+int oracle_bfs(int64_t n, const int64_t *R, const int32_t *C, int32_t src,
+               int32_t *depth, int32_t *pred)
+{
+    if (n <= 0 || src < 0 || src >= n) return 1;
+    int32_t *queue = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!queue) return 2;
+    for (int64_t v = 0; v < n; ++v) {
+        depth[v] = -1;
+        if (pred) pred[v] = -1;
+    }
+    int64_t head = 0, tail = 0;
+    depth[src] = 0;
+    if (pred) pred[src] = src;
+    queue[tail++] = src;
+    while (head < tail) {
+        int32_t u = queue[head++];
+        for (int64_t e = R[u]; e < R[u + 1]; ++e) {
+            int32_t v = C[e];
+            if (depth[v] == -1) {
+                depth[v] = depth[u] + 1;
+                if (pred) pred[v] = u;
+                queue[tail++] = v;
+            }
+        }
+    }
+    free(queue);
+    return 0;
+}
+
+/* ---- binary min-heap of (key = dist, vertex) with lazy deletion ---------- */
+typedef struct { uint64_t d; int32_t v; } heap_item;
+
+static void heap_push(heap_item *h, int64_t *size, heap_item x)
+{
+    int64_t i = (*size)++;
+    while (i > 0) {
+        int64_t p = (i - 1) / 2;
+        if (h[p].d <= x.d) break;
+        h[i] = h[p];
+        i = p;
+    }
+    h[i] = x;
+}
+
+static heap_item heap_pop(heap_item *h, int64_t *size)
+{
+    heap_item top = h[0];
+    heap_item last = h[--(*size)];
+    int64_t i = 0, s = *size;
+    for (;;) {
+        int64_t l = 2 * i + 1, r = l + 1, c = i;
+        uint64_t cd = last.d;
+        if (l < s && h[l].d < cd) { c = l; cd = h[l].d; }
+        if (r < s && h[r].d < cd) { c = r; }
+        if (c == i) break;
+        h[i] = h[c];
+        i = c;
+    }
+    if (s > 0) h[i] = last;
+    return top;
+}
+
+int oracle_sssp(int64_t n, const int64_t *R, const int32_t *C, const uint32_t *W,
+                int32_t src, uint32_t *dist_out, int32_t *pred)
+{
+    if (n <= 0 || src < 0 || src >= n || !W) return 1;
+    int64_t m = R[n];
+    uint64_t *dist = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+    unsigned char *done = (unsigned char *)calloc((size_t)n, 1);
+    /* every successful relaxation pushes one item: at most m + 1 live items */
+    heap_item *heap = (heap_item *)malloc((size_t)(m + 1) * sizeof(heap_item));
+    if (!dist || !done || !heap) { free(dist); free(done); free(heap); return 2; }
+    const uint64_t INF = UINT64_MAX;
+    for (int64_t v = 0; v < n; ++v) {
+        dist[v] = INF;
+        if (pred) pred[v] = -1;
+    }
+    int64_t size = 0;
+    dist[src] = 0;
+    if (pred) pred[src] = src;
+    heap_item s0 = {0, src};
+    heap_push(heap, &size, s0);
+    while (size > 0) {
+        heap_item it = heap_pop(heap, &size);
+        int32_t u = it.v;
+        if (done[u] || it.d != dist[u]) continue; /* stale entry */
+        done[u] = 1;
+        for (int64_t e = R[u]; e < R[u + 1]; ++e) {
+            int32_t v = C[e];
+            uint64_t nd = dist[u] + (uint64_t)W[e];
+            if (nd < dist[v]) {
+                dist[v] = nd;
+                if (pred) pred[v] = u;
+                heap_item x = {nd, v};
+                heap_push(heap, &size, x);
+            }
+        }
+    }
+    int rc = 0;
+    for (int64_t v = 0; v < n; ++v) {
+        if (dist[v] == INF) dist_out[v] = UINT32_MAX;
+        else if (dist[v] >= (uint64_t)UINT32_MAX) { rc = 3; dist_out[v] = UINT32_MAX; }
+        else dist_out[v] = (uint32_t)dist[v];
+    }
+    free(dist); free(done); free(heap);
+    return rc;
+}
