@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: BFS GTEPS on the BASELINE.json configs (default: config 2,
+direction-optimizing push-pull BFS on a kron_g500-logn21-shaped Kronecker
+graph), plus the roofline of the dominant kernel, a CPU-oracle baseline and an
+end-to-end number through the C ABI with host output buffers.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2_kron21]
+                    [--prim bfs|sssp] [--direction auto|push|pull]
+                    [--impl ours|reference] [--no-cpu-baseline]
+
+One "step" = one full traversal (every level of the hot path)
+from one seeded source, inputs resident in HBM. K steps cycle through K
+seeded sources (degree >= 1). L2 is flushed (a 256 MiB write) between
+timed steps, outside each step's CUDA-event bracket.
+Multi-GPU (torchrun, N>1): sources are independent problems, sharded across
+ranks (weak scaling; each rank owns the whole graph), no collective on the
+data path; value = edges traversed by all ranks / max-over-ranks time.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "BFS/SSSP GTEPS at 1/2/4/8 B200; achieved HBM GB/s as fraction of roofline"
+CONFIG_DESC = {
+    "c1_rmat16": "R-MAT scale 16, edge factor 16, unpermuted, BFS from vertex 0",
+    "c2_kron21": "Kronecker (Graph500 A,B,C=.57,.19,.19) scale 21, edge factor 48, permuted, "
+                 "symmetrised (kron_g500-logn21 shape)",
+    "c3_orkut": "Chung-Lu n=3,072,441, ~234M directed edges, weights U{1..64} (soc-orkut shape)",
+    "c4_road": "row-connected mesh 4899^2, p_vertical=0.2, weights U{1..64} (road_usa shape)",
+    "c5_kron25": "Graph500 Kronecker scale 25, edge factor 16, permuted, symmetrised",
+}
+PAPER_CONTEXT = {  # Table 3, K40c, real datasets: context only
+    ("c2_kron21", "bfs"): "Gunrock BFS kron_g500-logn21 on K40c: 19.15 ms, 9.51 GTEPS (P:1146-1147)",
+    ("c3_orkut", "bfs"): "Gunrock BFS soc-orkut on K40c: 47.23 ms, 4.50 GTEPS (P:1140-1141)",
+    ("c3_orkut", "sssp"): "Gunrock SSSP soc-orkut on K40c: 1088 ms, 0.1955 GTEPS (P:1152-1153)",
+    ("c4_road", "bfs"): "Gunrock BFS roadnet_CA (11x fewer edges) on K40c: 0.178 GTEPS (P:1150-1151)",
+    ("c4_road", "sssp"): "Gunrock SSSP roadnet_CA on K40c: 0.0249 GTEPS (P:1162-1163)",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=16)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2_kron21", choices=sorted(CONFIG_DESC))
+    ap.add_argument("--prim", default="bfs", choices=["bfs", "sssp"])
+    ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
+    ap.add_argument("--delta", type=int, default=0)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks sampler
+
+class Clocks:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, val in zip(names, p[5:9]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- byte model
+
+def algorithmic_bytes(stats, n, prim):
+    """SURVEY §8(d) algorithmic HBM bytes of one traversal from its per-level
+    records (4-byte words; bitmap probes are L2 traffic and not counted):
+      push level  12 f + 4 m_f + 12 d
+      pull level  n/8 + 8 u + 4 e_insp + 8 d + n/8
+      SSSP relax  16 f + 8 e + 12 r ;  far re-split 8 |far|
+      per run     8 n (depth/pred init) [+ 12 n for SSSP (dist/pred + stamp)]
+    """
+    B = 8 * n if prim == "bfs" else 12 * n
+    for r in stats["levels"]:
+        f, mf, d, ins = r["frontier"], r["frontier_edges"], r["discovered"], r["inspected_edges"]
+        if r["direction"] == 1:
+            B += 12 * f + 4 * mf + 12 * d
+        elif r["direction"] == 2:
+            B += n / 8 + 8 * r["aux"] + 4 * ins + 8 * d + n / 8
+        elif r["direction"] == 3:
+            B += 16 * f + 8 * mf + 12 * d
+        else:
+            B += 8 * f
+    return B
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy, burst)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------- reference arm
+
+def run_reference(args, rank, world):
+    """The CPU oracle as it stands, timed on this box's host cores (rank 0)."""
+    import numpy as np
+    import torch
+
+    import graphgen as gg
+    import oracle
+    if rank != 0:
+        return
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    g = gg.make_config(args.config, device=dev)
+    R, C, W = g.numpy()
+    srcs = [0] if args.config == "c1_rmat16" else gg.sources(g, args.warmup + args.steps)
+    srcs = (srcs * (args.warmup + args.steps))[: args.warmup + args.steps]
+    edges, secs = 0, 0.0
+    for i, s in enumerate(srcs):
+        t0 = time.perf_counter()
+        if args.prim == "bfs":
+            x, _ = oracle.bfs(R, C, s, want_pred=True)
+            unreached = -1
+        else:
+            x, _ = oracle.sssp(R, C, W, s, want_pred=True)
+            unreached = oracle.UINT32_MAX
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            edges += oracle.reached_edges(R, x, unreached)
+            secs += dt
+    value = edges / secs / 1e9
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "int32" if args.prim == "bfs" else "u32", "data": "synthetic",
+           "config": {"workload": "%s %s" % (args.config, args.prim), "graph": CONFIG_DESC[args.config],
+                      "n": g.n, "m": g.m},
+           "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                            "sample": "%d %s traversals of %s (one per step), single-threaded C oracle"
+                                      % (args.steps, args.prim, args.config)},
+           "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import graphgen as gg
+    import paper_1501_05387_b200 as gr
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    dev = torch.device("cuda", local)
+    want_w = args.prim == "sssp"
+    g = gg.make_config(args.config, device=dev, weights=want_w or None)
+    G = gr.Graph(g.R, g.C, g.W if want_w else None, symmetric=True)
+    deg = (g.R[1:] - g.R[:-1])
+    n, m = g.n, g.m
+    nsrc = args.warmup + args.steps * world
+    if args.config == "c1_rmat16":
+        all_srcs = [0] * nsrc
+    else:
+        all_srcs = gg.sources(g, nsrc)
+    warm_srcs = all_srcs[: args.warmup]
+    my_srcs = all_srcs[args.warmup + rank * args.steps: args.warmup + (rank + 1) * args.steps]
+
+    depth = torch.empty(n, dtype=torch.int32, device=dev)
+    pred = torch.empty(n, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(s, direction=args.direction):
+        if args.prim == "bfs":
+            G.bfs(s, depth, pred, direction=direction)
+        else:
+            G.sssp(s, depth, pred, delta=args.delta)
+
+    def reached(x):
+        if args.prim == "bfs":
+            return int(deg[x >= 0].sum())
+        return int(deg[x != -1].sum())  # uint32 max reads as -1 in int32
+
+    for s in warm_srcs:
+        step(s)
+    torch.cuda.synchronize()
+
+    def timed(srcs, direction):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in srcs]
+        edges, recs = 0, []
+        for (e0, e1), s in zip(ev, srcs):
+            flush.zero_()
+            e0.record(stream)
+            step(s, direction)
+            e1.record(stream)
+            edges += reached(depth)
+            recs.append(G.run_stats())
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in ev]
+        return edges, ms, recs
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = gr.gr_kernel_launch_count()
+    with Clocks(local) as clk:
+        edges, ms, recs = timed(my_srcs, args.direction)
+    launches = gr.gr_kernel_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot_ms = sum(ms)
+    if world > 1:
+        t = torch.tensor([tot_ms, float(edges)], dtype=torch.float64, device=dev)
+        tmax = t.clone()
+        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        tot_ms_all, edges_all = float(tmax[0]), float(t[1])
+    else:
+        tot_ms_all, edges_all = tot_ms, float(edges)
+    value = edges_all / (tot_ms_all * 1e-3) / 1e9
+
+    peak, peak_src = load_peaks()
+    byts = [algorithmic_bytes(r, n, args.prim) for r in recs]
+    kname = "bfs_kernel" if args.prim == "bfs" else "sssp_kernel"
+    achieved = sum(byts) / (tot_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
+                "bytes_per_launch": sum(byts) / len(byts),
+                "model": "SURVEY 8(d) algorithmic bytes from per-level run stats (push 12f+4m_f+12d; "
+                         "pull n/4+8u+4e_insp+8d; +8n init); one launch per traversal"}
+
+    out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": tot_ms_all / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None,
+           "dtype": "int32" if args.prim == "bfs" else "u32", "data": "synthetic",
+           "config": {"workload": "%s %s direction=%s" % (args.config, args.prim, args.direction),
+                      "graph": CONFIG_DESC[args.config], "n": n, "m": m,
+                      "sources": "%d seeded sources with degree>=1 per rank (S:519)" % args.steps,
+                      "l2": "flushed (256 MiB write) between timed steps",
+                      "parallelism": "replicas: sources sharded over %d rank(s)" % world},
+           "roofline": roofline, "gpu_launches": launches}
+    if rank == 0:
+        out["clocks"] = clk.summary()
+        out["paper_context"] = PAPER_CONTEXT.get((args.config, args.prim))
+        out["levels_per_step"] = statistics.mean(r["num_levels"] for r in recs)
+
+    # ---- end to end through the C ABI with host buffers (rank 0 measures; all ranks run)
+    pin_d = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    pin_p = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    e2e_edges, e2e_s = 0, 0.0
+    for s in my_srcs:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if args.prim == "bfs":
+            G.bfs(s, pin_d, pin_p, direction=args.direction)
+        else:
+            G.sssp(s, pin_d, pin_p, delta=args.delta)
+        e2e_s += time.perf_counter() - t0
+        e2e_edges += reached(pin_d.to(dev))
+    out["e2e"] = {"value": e2e_edges / e2e_s / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                  "d2h_bytes_per_step": 8 * n,
+                  "what": "gr_bfs/gr_sssp through the C ABI writing host (pinned) depth+pred; "
+                          "host wall clock per call; graph resident (created once, P:1089-1090)"}
+
+    if rank == 0 and not args.no_extras and args.prim == "bfs" and args.direction == "auto":
+        # the push-only roofline row of the north star (same sources)
+        pe, pms, precs = timed(my_srcs, "push")
+        pb = [algorithmic_bytes(r, n, "bfs") for r in precs]
+        pach = sum(pb) / (sum(pms) * 1e-3) / 1e9
+        out["push_only"] = {"value": pe / (sum(pms) * 1e-3) / 1e9, "unit": "GTEPS",
+                            "ms_per_step": sum(pms) / len(pms), "achieved_gbs": pach,
+                            "frac": pach / peak}
+
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        R, C, W = g.numpy()
+        ce, cs, cnt = 0, 0.0, 0
+        for s in my_srcs:
+            t0 = time.perf_counter()
+            if args.prim == "bfs":
+                x, _ = oracle.bfs(R, C, s)
+                un = -1
+            else:
+                x, _ = oracle.sssp(R, C, W, s)
+                un = oracle.UINT32_MAX
+            cs += time.perf_counter() - t0
+            ce += oracle.reached_edges(R, x, un)
+            cnt += 1
+            if cs > args.cpu_sample_s:
+                break
+        out["cpu_baseline"] = {"value": ce / cs / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                               "sample": "%d of the timed sources, full %s traversals of %s, "
+                                         "single-threaded C oracle (%d host cores available)"
+                                         % (cnt, args.prim, args.config, os.cpu_count())}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    G.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,193 @@
+/*
+ * gr.h -- C ABI of the B200-native frontier library (BFS / SSSP hot path of
+ * Gunrock, Wang et al., PPoPP'16, arXiv 1501.05387).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; "S:n" = SPEC.md line n;
+ * "A-k" = a reading of the paper listed in DESIGN.md "Readings".
+ *
+ * Conventions for every entry point
+ *  - C99, no C++ types, no torch types. Status codes only; no exception
+ *    crosses the boundary. On failure gr_last_error() returns a message
+ *    (thread-local, valid until the next call on that thread) and outputs are
+ *    unspecified.
+ *  - Pointers may be host or device memory; the library detects which with
+ *    cudaPointerGetAttributes. Device outputs (e.g. a torch tensor's
+ *    data_ptr()) are written in place; host outputs are filled by a
+ *    device->host copy at the end of the call.
+ *  - Every call is synchronous with respect to the host. All device work is
+ *    enqueued on the stream given to gr_graph_create (or gr_graph_set_stream).
+ *  - One traversal at a time per gr_graph (the scratch space is per graph,
+ *    cf. S:177 "A single traversal run is not reentrant"). Distinct graphs are
+ *    independent. The library never retains a caller pointer after returning.
+ */
+#ifndef GR_H_
+#define GR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GR_OK = 0,
+    GR_ERR_INVALID_ARGUMENT = 1, /* NULL pointer, n <= 0, bad option value        */
+    GR_ERR_INVALID_GRAPH = 2,    /* CSR invariant broken; message names the index  */
+    GR_ERR_OUT_OF_RANGE = 3,     /* src not in [0, n)                     */
+    GR_ERR_NO_WEIGHTS = 4,       /* gr_sssp on a graph created without weights */
+    GR_ERR_OVERFLOW = 5,         /* a distance could exceed UINT32_MAX-1 (A-19), or
+                                    a queue capacity would be exceeded             */
+    GR_ERR_OUT_OF_MEMORY = 6,
+    GR_ERR_CUDA = 7,             /* a CUDA runtime error; message has the detail   */
+    GR_ERR_NCCL = 8
+} gr_status;
+
+typedef struct gr_graph gr_graph; /* opaque; immutable topology after create */
+
+/* gr_graph_create flags */
+enum {
+    GR_SYMMETRIC = 1u << 0, /* caller asserts (u,v) in E <=> (v,u) in E (the paper's
+                               undirected inputs); pull then
+                               reads the CSR as its own CSC. Without it the library
+                               builds the reverse graph (CSC) on the device (A-18). */
+    GR_VALIDATE = 1u << 2   /* O(n+m) CSR checks on the device:
+                               R[0]=0, R non-decreasing, R[n]=m, 0<=C[e]<n.       */
+};
+
+/*
+ * gr_graph_create -- build the device graph G=(V,E,w_e) from a CSR
+ * (§3 "A graph is an ordered pair G=(V,E,w_e,w_v)"
+ * "CSR uses a column-indices array, C, ... and a row-offsets array, R").
+ *   n            number of vertices, >= 1 (n <= 2^31-1)
+ *   m            number of directed edges, >= 0
+ *   row_offsets  int64[n+1]: neighbours of v are col_indices[R[v] .. R[v+1])
+ *   col_indices  int32[m], each in [0, n). Self-loops and parallel edges are
+ *                allowed (BFS ignores them; SSSP takes the minimum weight).
+ *   weights      uint32[m] non-negative edge weights w_e, or NULL
+ *                for a BFS-only graph.
+ *   flags        GR_SYMMETRIC | GR_VALIDATE
+ *   device       CUDA device ordinal the graph lives on
+ *   cuda_stream  cudaStream_t to enqueue all work on (NULL = legacy stream)
+ *   out          receives the handle
+ * All inputs are copied; the caller may free them on return. Graph creation is
+ * outside the timed region of every benchmark ("All results
+ * ignore transfer time").
+ * Errors: GR_ERR_INVALID_ARGUMENT, GR_ERR_INVALID_GRAPH (first bad index named,
+ * e.g. "R[17]=5 < R[16]=9" or "C[1234]=70000 >= n"), GR_ERR_OUT_OF_MEMORY,
+ * GR_ERR_CUDA.
+ */
+gr_status gr_graph_create(int64_t n, int64_t m, const int64_t *row_offsets,
+                          const int32_t *col_indices, const uint32_t *weights,
+                          uint32_t flags, int device, void *cuda_stream,
+                          gr_graph **out);
+
+/* Frees all device memory owned by g. NULL is a no-op. */
+gr_status gr_graph_destroy(gr_graph *g);
+
+/* Re-targets subsequent work of g to another stream on the same device. */
+gr_status gr_graph_set_stream(gr_graph *g, void *cuda_stream);
+
+typedef struct {
+    int64_t n, m;
+    int64_t max_degree;      /* max out-degree                                  */
+    int64_t nonisolated;     /* vertices with in-degree > 0 (pull candidates)   */
+    int32_t symmetric;       /* 1 if created with GR_SYMMETRIC                  */
+    int32_t has_weights;
+    uint32_t max_weight;
+    int32_t device;
+    int64_t device_bytes;    /* device memory currently owned by the graph      */
+} gr_graph_info;
+
+gr_status gr_graph_info_get(const gr_graph *g, gr_graph_info *out);
+
+/*
+ * gr_bfs -- breadth-first search from src (§5.1: "BFS initializes
+ * its vertex frontier with a single source vertex. On each iteration, it
+ * generates a new frontier of vertices with all unvisited neighbor vertices
+ * in the current frontier, setting their depths"). Each level is one
+ * bulk-synchronous step: a fused advance+filter
+ * (push) or a pull advance over in-edges.
+ *   src        source vertex in [0, n)
+ *   depth_out  int32[n]: hop distance from src following out-edges, -1 when
+ *              unreached (A-2). Deterministic.
+ *   pred_out   int32[n] or NULL: a valid BFS parent (pred[v] -> v is an edge
+ *              and depth[pred[v]] = depth[v]-1), pred[src] = src (A-1), -1 when
+ *              unreached. Which valid parent is nondeterministic.
+ *   opts       NULL = defaults (all zero fields = defaults)
+ * Errors: GR_ERR_OUT_OF_RANGE for src outside [0,n); GR_ERR_INVALID_ARGUMENT.
+ */
+typedef struct {
+    int32_t direction;   /* 0 auto (direction-optimizing), 1 push only, 2 pull only */
+    int32_t strategy;    /* 0 auto, 1 thread/warp/CTA (node-granular), 2 merge-path LB
+                            over edges (threshold reading A-4)            */
+    int32_t idempotent;  /* 0 = exactly-once claim (atomicOr on the visited bitmap,
+                            P:800-802); 1 = atomic-free idempotent discovery with
+                            culling heuristics (A-5, A-6)    */
+    int32_t switch_rule; /* 0 Beamer alpha/beta (default), 1 paper-literal
+                            "unvisited < frontier" (A-3)                */
+    double alpha, beta;  /* Beamer parameters; 0 = 14, 24                          */
+    int64_t lb_threshold;/* frontier size at which auto strategy switches from
+                            node-granular to edge-granular balancing; 0 = default   */
+} gr_bfs_opts;
+
+gr_status gr_bfs(gr_graph *g, int32_t src, int32_t *depth_out, int32_t *pred_out,
+                 const gr_bfs_opts *opts);
+
+/*
+ * gr_sssp -- single-source shortest paths with non-negative integer weights,
+ * delta-stepping with Gunrock's two-level near/far priority queue
+ * (Alg. 1; §5.2; priority queue P:838-857).
+ *   dist_out  uint32[n]: exact shortest distance, UINT32_MAX when unreached
+ *             (A-2). Deterministic.
+ *   pred_out  int32[n] or NULL: a tight parent (dist[pred[v]] + w = dist[v]),
+ *             pred[src] = src, -1 when unreached (A-9).
+ *   opts      NULL = defaults; delta = 0 picks a delta from graph statistics.
+ * Errors: GR_ERR_NO_WEIGHTS, GR_ERR_OUT_OF_RANGE, GR_ERR_OVERFLOW (if
+ * max_w*(n-1) >= UINT32_MAX, A-19), GR_ERR_INVALID_ARGUMENT.
+ */
+typedef struct {
+    uint32_t delta;      /* near/far band width; 0 = auto; UINT32_MAX = one band
+                            (Bellman-Ford-like)                                    */
+    int32_t strategy;    /* as gr_bfs_opts.strategy                                */
+} gr_sssp_opts;
+
+gr_status gr_sssp(gr_graph *g, int32_t src, uint32_t *dist_out, int32_t *pred_out,
+                  const gr_sssp_opts *opts);
+
+/* Per-level records of the last gr_bfs / gr_sssp on g (SURVEY §5 tracing). */
+typedef struct {
+    int32_t level;           /* BFS level or SSSP iteration                        */
+    int32_t direction;       /* 1 push, 2 pull, 3 SSSP relax, 4 SSSP far re-split  */
+    int64_t frontier;        /* |frontier| (queue entries)                         */
+    int64_t frontier_edges;  /* sum of out-degrees of the frontier                 */
+    int64_t discovered;      /* vertices discovered / improved-and-queued          */
+    int64_t inspected_edges; /* edges actually read (push: frontier_edges; pull:
+                                up to the first frontier hit, early exit)          */
+    int64_t aux;             /* SSSP: far-queue size; BFS: unvisited (heuristic u) */
+} gr_level_stats;
+
+typedef struct {
+    int32_t num_levels;            /* levels executed (may exceed records kept)    */
+    int32_t num_records;           /* records available in levels[]                */
+    const gr_level_stats *levels;  /* valid until the next run / destroy           */
+    int64_t reached;               /* vertices reached                             */
+    uint32_t delta;                /* SSSP: delta used                             */
+    int32_t kernel_launches;       /* kernels launched by the last run            */
+} gr_run_stats;
+
+gr_status gr_get_run_stats(gr_graph *g, gr_run_stats *out);
+
+/* Message for the last failure on the calling thread ("" if none). */
+const char *gr_last_error(void);
+
+/* Kernels this process has launched through the library (all graphs). */
+uint64_t gr_kernel_launch_count(void);
+
+/* Library version string, e.g. "gr_b200 0.1 sm_100a". */
+const char *gr_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GR_H_ */

@@ -1,0 +1,142 @@
+// gr_internal.cuh -- shared device/host internals of the B200 frontier library.
+// Not part of the ABI (include/gr.h is). Citations: P:n = PAPER.md line n.
+#pragma once
+
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/gr.h"
+
+namespace gr {
+
+namespace cg = cooperative_groups;
+
+constexpr int kWarp = 32;
+constexpr int kBlock = 256;              // threads per CTA of the persistent kernels
+constexpr int kWarpsPerBlock = kBlock / kWarp;
+constexpr int kStageCap = 64;            // per-warp smem staging of appended vertices
+constexpr int kMaxStatRecords = 1 << 16; // per-level records kept for gr_get_run_stats
+constexpr int kSlots = 4;                // rotating per-level control slots
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(const char *fmt, ...);
+gr_status cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define GR_CUDA(call)                                                             \
+    do {                                                                          \
+        cudaError_t e_ = (call);                                                  \
+        if (e_ != cudaSuccess) return ::gr::cuda_fail(e_, #call, __FILE__, __LINE__); \
+    } while (0)
+
+void count_launch(int k = 1);
+
+// ---------------------------------------------------------------- control block
+// One slot per in-flight level (rotating, kSlots). Level L reads the frontier
+// descriptor of slot L%4, writes that of slot (L+1)%4, and resets slot
+// (L+2)%4 (which no block reads or writes during level L).
+struct Slot {
+    unsigned long long qpack;   // frontier queue: (sum of degrees << S) | count
+    unsigned long long ndisc;   // vertices discovered / queued in this step
+    unsigned long long fpack;   // SSSP far appends (count) during this step
+    unsigned long long work;    // dynamic work counter
+    unsigned long long minfar;  // SSSP re-split: min far distance
+    unsigned long long insp;    // edges inspected in this step
+    unsigned long long pad[2];
+};
+
+struct Ctl {
+    Slot slot[kSlots];
+    unsigned long long overflow;   // set when a queue capacity would be exceeded
+    unsigned long long levels;     // levels executed by the last run
+    unsigned long long reached;    // (unused by kernels; host bookkeeping)
+    unsigned long long far_count[2];
+    unsigned long long pad[3];
+};
+
+// ---------------------------------------------------------------- graph object
+struct Graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n = 0, m = 0;
+    bool symmetric = false;
+    bool has_w = false;
+    uint32_t max_w = 0;
+    int64_t max_deg = 0, nonisolated = 0;
+    int pack_shift = 32;          // S: bits of the count field in Slot::qpack
+
+    // topology (device)
+    int64_t *R = nullptr;         // [n+1]
+    int32_t *C = nullptr;         // [m]
+    uint32_t *W = nullptr;        // [m] or null
+    int64_t *Rt = nullptr;        // CSC (== R when symmetric)
+    int32_t *Ct = nullptr;
+
+    // per-run scratch (device)
+    uint32_t *visited = nullptr;  // [nwords] visited bitmap (P:793-799 culling)
+    uint32_t *fbuf[2] = {nullptr, nullptr}; // frontier bitmaps for pull
+    int32_t *qv[2] = {nullptr, nullptr};    // frontier queues (vertex ids)
+    int64_t *qo[2] = {nullptr, nullptr};    // exclusive prefix of degrees
+    int32_t *depth_buf = nullptr; // internal outputs when caller passes host memory
+    int32_t *pred_buf = nullptr;
+    uint32_t *dist_buf = nullptr;
+    // SSSP scratch
+    unsigned long long *dp = nullptr; // packed (dist << 32) | pred  (A-9)
+    int32_t *stamp = nullptr;         // RemoveRedundant stamp (A-7)
+    int32_t *farq[2] = {nullptr, nullptr};
+    int64_t far_cap = 0;
+
+    Ctl *ctl = nullptr;
+    gr_level_stats *stats_dev = nullptr;
+    gr_level_stats *stats_host = nullptr;
+    int stats_levels = 0, stats_records = 0;
+    int64_t reached = 0;
+    uint32_t last_delta = 0;
+    int last_launches = 0;
+    int64_t bytes = 0;
+
+    int num_sms = 148;
+    int nwords() const { return (int)((n + 31) / 32); }
+};
+
+gr_status dev_alloc(Graph *g, void **p, size_t bytes);
+void dev_free_all(Graph *g);
+
+// ---------------------------------------------------------------- device helpers
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// L2-coherent load (bypasses L1): used for state that other SMs update
+// within the same step (visited bitmap, distances).
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p) {
+    return __ldcg(p);
+}
+__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
+    return *(volatile const unsigned long long *)p;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T x) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T y = __shfl_up_sync(0xffffffffu, x, d);
+        if ((int)lane_id() >= d) x += y;
+    }
+    return x;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T x) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+    return x;
+}
+
+}  // namespace gr

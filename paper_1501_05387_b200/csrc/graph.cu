@@ -1,0 +1,237 @@
+// graph.cu -- device graph store (a1 of SURVEY §8(a)): CSR ingest, optional
+// validation, reverse graph (CSC) for pull on directed inputs, degree stats,
+// per-run scratch. P:237-244 (graph definition), P:267-278 (SOA + CSR),
+// P:821-825 (bitmaps), S:31-34 / S:45 (CSR invariants, error naming the index).
+#include <cub/cub.cuh>
+
+#include "gr_internal.cuh"
+
+namespace gr {
+
+gr_status dev_alloc(Graph *g, void **p, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        set_error("cudaMalloc of %zu bytes failed (out of device memory)", bytes);
+        return GR_ERR_OUT_OF_MEMORY;
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc", __FILE__, __LINE__);
+    g->bytes += (int64_t)bytes;
+    return GR_OK;
+}
+
+void dev_free_all(Graph *g) {
+    void *ptrs[] = {g->R, g->C, g->W, (g->Rt != g->R) ? g->Rt : nullptr,
+                    (g->Ct != g->C) ? g->Ct : nullptr, g->visited, g->fbuf[0], g->fbuf[1],
+                    g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->depth_buf, g->pred_buf,
+                    g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+    if (g->stats_host) cudaFreeHost(g->stats_host);
+}
+
+// ---------------------------------------------------------------- validation
+// err[0] = first bad row-offset index (or INT64_MAX), err[1] = first bad edge.
+__global__ void validate_kernel(const int64_t *R, const int32_t *C, int64_t n, int64_t m,
+                                unsigned long long *err) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = tid; i <= n; i += nt) {
+        bool bad = (i == 0) ? (R[0] != 0) : (R[i] < R[i - 1]);
+        if (i == n && R[n] != m) bad = true;
+        if (bad) atomicMin(err, (unsigned long long)i);
+    }
+    for (int64_t e = tid; e < m; e += nt) {
+        int32_t c = C[e];
+        if (c < 0 || c >= n) atomicMin(err + 1, (unsigned long long)e);
+    }
+}
+
+__global__ void degree_stats_kernel(const int64_t *R, const int64_t *Rt, int64_t n,
+                                    unsigned long long *maxdeg, unsigned long long *noniso) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long mx = 0, cnt = 0;
+    for (int64_t v = tid; v < n; v += nt) {
+        unsigned long long d = (unsigned long long)(R[v + 1] - R[v]);
+        mx = d > mx ? d : mx;
+        cnt += (Rt[v + 1] > Rt[v]) ? 1 : 0;
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+        unsigned long long o = __shfl_xor_sync(0xffffffffu, mx, s);
+        mx = o > mx ? o : mx;
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, s);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(maxdeg, mx);
+        atomicAdd(noniso, cnt);
+    }
+}
+
+__global__ void max_weight_kernel(const uint32_t *W, int64_t m, unsigned int *out) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    unsigned int mx = 0;
+    for (int64_t e = tid; e < m; e += nt) mx = max(mx, W[e]);
+    for (int s = 16; s > 0; s >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, s));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, mx);
+}
+
+// reverse graph: in-degree count, scan, scatter (order within a list is free)
+__global__ void indeg_kernel(const int32_t *C, int64_t m, unsigned long long *cnt) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = tid; e < m; e += nt) atomicAdd(cnt + C[e], 1ull);
+}
+
+__global__ void csc_scatter_kernel(const int64_t *R, const int32_t *C, int64_t n,
+                                   unsigned long long *cursor, int32_t *Ct) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t u = tid; u < n; u += nt)
+        for (int64_t e = R[u]; e < R[u + 1]; ++e) {
+            unsigned long long p = atomicAdd(cursor + C[e], 1ull);
+            Ct[p] = (int32_t)u;
+        }
+}
+
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static int bits_for(int64_t x) {  // smallest S with x < 2^S
+    int s = 1;
+    while (s < 62 && (x >> s) != 0) ++s;
+    return s;
+}
+
+gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C, const uint32_t *W,
+                       uint32_t flags, int device, void *stream, Graph **out) {
+    if (!out) { set_error("out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
+    *out = nullptr;
+    if (n <= 0 || n > 0x7fffffffLL) { set_error("n=%lld must be in [1, 2^31-1]", (long long)n); return GR_ERR_INVALID_ARGUMENT; }
+    if (m < 0) { set_error("m=%lld < 0", (long long)m); return GR_ERR_INVALID_ARGUMENT; }
+    if (!R || (m > 0 && !C)) { set_error("row_offsets / col_indices is NULL"); return GR_ERR_INVALID_ARGUMENT; }
+    GR_CUDA(cudaSetDevice(device));
+    Graph *g = new Graph();
+    g->device = device;
+    g->stream = (cudaStream_t)stream;
+    g->n = n; g->m = m;
+    g->symmetric = (flags & GR_SYMMETRIC) != 0;
+    g->has_w = W != nullptr;
+    GR_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
+    gr_status st;
+#define TRY(x) do { st = (x); if (st != GR_OK) { dev_free_all(g); delete g; return st; } } while (0)
+#define TRYC(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { st = cuda_fail(e_, #x, __FILE__, __LINE__); dev_free_all(g); delete g; return st; } } while (0)
+    cudaStream_t s = g->stream;
+    TRY(dev_alloc(g, (void **)&g->R, (n + 1) * sizeof(int64_t)));
+    TRY(dev_alloc(g, (void **)&g->C, m * sizeof(int32_t)));
+    TRYC(cudaMemcpyAsync(g->R, R, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, s));
+    if (m) TRYC(cudaMemcpyAsync(g->C, C, m * sizeof(int32_t), cudaMemcpyDefault, s));
+    if (W) {
+        TRY(dev_alloc(g, (void **)&g->W, m * sizeof(uint32_t)));
+        if (m) TRYC(cudaMemcpyAsync(g->W, W, m * sizeof(uint32_t), cudaMemcpyDefault, s));
+    }
+    unsigned long long *tmp = nullptr;  // 4 scratch words
+    TRY(dev_alloc(g, (void **)&tmp, 8 * sizeof(unsigned long long)));
+    g->bytes -= 8 * sizeof(unsigned long long);
+    const int blocks = g->num_sms * 8;
+    if (flags & GR_VALIDATE) {
+        unsigned long long init[2] = {~0ull, ~0ull}, res[2];
+        TRYC(cudaMemcpyAsync(tmp, init, sizeof(init), cudaMemcpyHostToDevice, s));
+        validate_kernel<<<blocks, 256, 0, s>>>(g->R, g->C, n, m, tmp);
+        count_launch();
+        TRYC(cudaMemcpyAsync(res, tmp, sizeof(res), cudaMemcpyDeviceToHost, s));
+        TRYC(cudaStreamSynchronize(s));
+        if (res[0] != ~0ull || res[1] != ~0ull) {
+            int64_t hv[2] = {0, 0};
+            if (res[0] != ~0ull) {
+                int64_t i = (int64_t)res[0];
+                TRYC(cudaMemcpy(hv, g->R + (i > 0 ? i - 1 : 0), (i > 0 ? 2 : 1) * sizeof(int64_t),
+                                cudaMemcpyDeviceToHost));
+                if (i == 0) set_error("R[0]=%lld != 0", (long long)hv[0]);
+                else if (hv[1] < hv[0]) set_error("R[%lld]=%lld < R[%lld]=%lld", (long long)i, (long long)hv[1], (long long)(i - 1), (long long)hv[0]);
+                else set_error("R[%lld]=%lld != m=%lld", (long long)i, (long long)hv[1], (long long)m);
+            } else {
+                int32_t c;
+                TRYC(cudaMemcpy(&c, g->C + res[1], sizeof(int32_t), cudaMemcpyDeviceToHost));
+                set_error("C[%llu]=%d not in [0, n=%lld)", res[1], c, (long long)n);
+            }
+            cudaFree(tmp);
+            dev_free_all(g);
+            delete g;
+            return GR_ERR_INVALID_GRAPH;
+        }
+    }
+    if (g->symmetric) {
+        g->Rt = g->R;
+        g->Ct = g->C;
+    } else {
+        TRY(dev_alloc(g, (void **)&g->Rt, (n + 1) * sizeof(int64_t)));
+        TRY(dev_alloc(g, (void **)&g->Ct, m * sizeof(int32_t)));
+        unsigned long long *cnt = nullptr;
+        TRY(dev_alloc(g, (void **)&cnt, (n + 1) * sizeof(unsigned long long)));
+        g->bytes -= (n + 1) * sizeof(unsigned long long);
+        TRYC(cudaMemsetAsync(cnt, 0, (n + 1) * sizeof(unsigned long long), s));
+        indeg_kernel<<<blocks, 256, 0, s>>>(g->C, m, cnt + 1);
+        count_launch();
+        size_t tb = 0;
+        TRYC(cub::DeviceScan::InclusiveSum(nullptr, tb, cnt + 1, (unsigned long long *)g->Rt + 1, (int)n, s));
+        void *tbuf = nullptr;
+        TRYC(cudaMalloc(&tbuf, tb));
+        TRYC(cub::DeviceScan::InclusiveSum(tbuf, tb, cnt + 1, (unsigned long long *)g->Rt + 1, (int)n, s));
+        TRYC(cudaMemsetAsync(g->Rt, 0, sizeof(int64_t), s));
+        TRYC(cudaMemcpyAsync(cnt, g->Rt, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+        csc_scatter_kernel<<<blocks, 256, 0, s>>>(g->R, g->C, n, cnt, g->Ct);
+        count_launch(2);
+        TRYC(cudaStreamSynchronize(s));
+        cudaFree(tbuf);
+        cudaFree(cnt);
+    }
+    {
+        unsigned long long zero[4] = {0, 0, 0, 0}, res[4];
+        TRYC(cudaMemcpyAsync(tmp, zero, sizeof(zero), cudaMemcpyHostToDevice, s));
+        degree_stats_kernel<<<blocks, 256, 0, s>>>(g->R, g->Rt, n, tmp, tmp + 1);
+        count_launch();
+        if (W && m) {
+            max_weight_kernel<<<blocks, 256, 0, s>>>(g->W, m, (unsigned int *)(tmp + 2));
+            count_launch();
+        }
+        TRYC(cudaMemcpyAsync(res, tmp, sizeof(res), cudaMemcpyDeviceToHost, s));
+        TRYC(cudaStreamSynchronize(s));
+        g->max_deg = (int64_t)res[0];
+        g->nonisolated = (int64_t)res[1];
+        g->max_w = (uint32_t)(res[2] & 0xffffffffu);
+    }
+    cudaFree(tmp);
+
+    // per-run scratch for BFS (SSSP scratch is allocated on first use)
+    const int64_t nw = (n + 31) / 32;
+    TRY(dev_alloc(g, (void **)&g->visited, nw * sizeof(uint32_t)));
+    TRY(dev_alloc(g, (void **)&g->fbuf[0], nw * sizeof(uint32_t)));
+    TRY(dev_alloc(g, (void **)&g->fbuf[1], nw * sizeof(uint32_t)));
+    for (int i = 0; i < 2; ++i) {
+        TRY(dev_alloc(g, (void **)&g->qv[i], n * sizeof(int32_t)));
+        TRY(dev_alloc(g, (void **)&g->qo[i], n * sizeof(int64_t)));
+    }
+    g->pack_shift = bits_for(n + 1);
+    TRY(dev_alloc(g, (void **)&g->ctl, sizeof(Ctl)));
+    TRYC(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s));
+    TRY(dev_alloc(g, (void **)&g->stats_dev, kMaxStatRecords * sizeof(gr_level_stats)));
+    TRYC(cudaMallocHost((void **)&g->stats_host, kMaxStatRecords * sizeof(gr_level_stats)));
+    TRYC(cudaStreamSynchronize(s));
+#undef TRY
+#undef TRYC
+    *out = g;
+    return GR_OK;
+}
+
+bool ptr_on_device(const void *p) { return is_device_ptr(p); }
+
+}  // namespace gr

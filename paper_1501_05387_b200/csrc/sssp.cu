@@ -1,0 +1,260 @@
+// sssp.cu -- single-source shortest paths, delta-stepping with Gunrock's
+// two-level near/far priority queue, as ONE persistent cooperative kernel.
+//
+// Paper: Alg. 1: UpdateLabel = "new_label < atomicMin(labels[d],
+// new_label)", SetPred, RemoveRedundant via an
+// output-queue stamp ("a bitmap flag array associated with the
+// frontier to remove redundant vertices" P:950-951); priority queue (P:838-857,
+// "an additional filter pass between two iterations" P:941-942).
+// Readings: A-7 (stamp keyed by iteration AND slice), A-8 (one fused relax
+// kernel step per iteration + far re-split pass), A-9 (64-bit packed
+// atomicMin keeps pred consistent with dist), A-10 (delta), A-11 (far pile:
+// drop stale, jump threshold to the band of the minimum far distance).
+#include "frontier.cuh"
+
+namespace gr {
+
+struct SsspArgs {
+    int64_t n, m;
+    const int64_t *R;
+    const int32_t *C;
+    const uint32_t *W;
+    unsigned long long *dp;   // (dist << 32) | pred
+    int32_t *stamp;
+    int32_t *qv0, *qv1;
+    int64_t *qo0, *qo1;
+    int32_t *far0, *far1;
+    int64_t far_cap;
+    Ctl *ctl;
+    gr_level_stats *stats;
+    int32_t src;
+    uint64_t delta;
+    int S;
+};
+
+// Fused advance + compute + filter of one near iteration (a10).
+struct RelaxOp {
+    unsigned long long *dp;
+    int32_t *stamp;
+    const uint32_t *W;
+    const int64_t *R;
+    uint64_t thr;
+    int32_t key_near;   // 2*it   (A-7)
+    Appender *nearq;
+    Appender *farq;
+    unsigned long long nimp;
+
+    __device__ __forceinline__ unsigned long long entry(int32_t v) {
+        return ld_cg(dp + v) >> 32;  // dist[u] read when the window is loaded
+    }
+
+    template <int U>
+    __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *du,
+                                          const int32_t *dst, const int64_t *eidx) {
+        uint32_t w[U];
+        unsigned long long cur[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            w[u] = ok[u] ? __ldg(W + eidx[u]) : 0u;
+            cur[u] = ok[u] ? ld_cg(dp + dst[u]) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            bool to_near = false, to_far = false;
+            int64_t deg = 0;
+            const int32_t v = dst[u];
+            const unsigned long long nd = du[u] + w[u];
+            if (ok[u] && nd < (cur[u] >> 32)) {
+                const unsigned long long pk = (nd << 32) | (unsigned int)src[u];
+                const unsigned long long old = atomicMin(dp + v, pk);
+                if (nd < (old >> 32)) {
+                    const bool far = nd >= thr;
+                    const int32_t key = key_near + (far ? 1 : 0);
+                    if (atomicExch(stamp + v, key) != key) {
+                        if (far) to_far = true;
+                        else { to_near = true; deg = R[v + 1] - R[v]; }
+                    }
+                    ++nimp;
+                }
+            }
+            nearq->push(to_near && deg > 0, v, deg);
+            farq->push(to_far, v, 0);
+        }
+    }
+};
+
+__global__ void __launch_bounds__(kBlock) sssp_kernel(SsspArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ int32_t s_v[kWarpsPerBlock][kStageCap];
+    __shared__ int64_t s_d[kWarpsPerBlock][kStageCap];
+    __shared__ int32_t s_fv[kWarpsPerBlock][kStageCap];
+
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gw = tid >> 5;
+    const int64_t nw = nthreads >> 5;
+    const int wib = threadIdx.x >> 5;
+    const unsigned long long cmask = (1ull << a.S) - 1;
+
+    // ---- Set_Problem_Data ----------------------------------------
+    for (int64_t v = tid; v < a.n; v += nthreads) {
+        a.dp[v] = ~0ull;   // dist = UINT32_MAX (inf), pred = -1
+        a.stamp[v] = -1;
+    }
+    if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) ((unsigned long long *)a.ctl->slot)[tid] = 0ull;
+    if (tid == 0) {
+        a.ctl->overflow = 0ull;
+        a.ctl->far_count[0] = 0ull;
+        a.ctl->far_count[1] = 0ull;
+    }
+    grid.sync();
+    if (tid < kSlots) a.ctl->slot[tid].minfar = ~0ull;
+    if (tid == 0) {
+        const int64_t d = a.R[a.src + 1] - a.R[a.src];
+        a.dp[a.src] = (unsigned long long)(unsigned int)a.src;  // dist 0, pred = src (A-1)
+        if (d > 0) {
+            a.qv0[0] = a.src;
+            a.qo0[0] = 0;
+            a.ctl->slot[0].qpack = ((unsigned long long)d << a.S) | 1ull;
+        }
+    }
+    grid.sync();
+
+    Appender nearq, farq;
+    nearq.sv = s_v[wib]; nearq.sd = s_d[wib]; nearq.cnt = 0; nearq.S = a.S; nearq.cap = a.n;
+    nearq.overflow = &a.ctl->overflow;
+    farq.sv = s_fv[wib]; farq.sd = nullptr; farq.cnt = 0; farq.qo = nullptr; farq.S = 0;
+    farq.cap = a.far_cap; farq.overflow = &a.ctl->overflow;
+
+    uint64_t thr = a.delta;          // near band is [.., thr)
+    int32_t it = 0;                  // stamp iteration (keys 2*it, 2*it+1)
+    int fp = 0;                      // current far buffer
+    int k = 0;                       // step index (slots, queue ping-pong)
+    for (;; ++k) {
+        Slot &cur = a.ctl->slot[k & 3];
+        Slot &nxt = a.ctl->slot[(k + 1) & 3];
+        const unsigned long long qp = ld_volatile(&cur.qpack);
+        const int64_t f = (int64_t)(qp & cmask);
+        const int64_t mf = (int64_t)(qp >> a.S);
+        const int64_t fc = (int64_t)ld_volatile(&a.ctl->far_count[fp]);
+        if (k > 0 && tid == 0 && k - 1 < kMaxStatRecords)
+            a.stats[k - 1].discovered = (int64_t)ld_volatile(&cur.ndisc);
+        if (ld_volatile(&a.ctl->overflow)) break;
+        if (f == 0 && fc == 0) break;
+        if (tid == 0) {
+            Slot &rst = a.ctl->slot[(k + 2) & 3];
+            rst.qpack = 0; rst.ndisc = 0; rst.fpack = 0; rst.work = 0; rst.minfar = ~0ull;
+            rst.insp = 0;
+            if (k < kMaxStatRecords) {
+                gr_level_stats &st = a.stats[k];
+                st.level = k; st.direction = f > 0 ? 3 : 4; st.frontier = f > 0 ? f : fc;
+                st.frontier_edges = mf; st.discovered = 0; st.inspected_edges = mf; st.aux = fc;
+            }
+        }
+        int32_t *qv_c = (k & 1) ? a.qv1 : a.qv0;
+        int64_t *qo_c = (k & 1) ? a.qo1 : a.qo0;
+        nearq.qv = (k & 1) ? a.qv0 : a.qv1;
+        nearq.qo = (k & 1) ? a.qo0 : a.qo1;
+        nearq.counter = &nxt.qpack;
+
+        if (f > 0) {
+            // ---- near iteration: Advance(UpdateLabel, SetPred) + Filter ----
+            ++it;
+            farq.qv = fp ? a.far1 : a.far0;
+            farq.counter = &a.ctl->far_count[fp];
+            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull};
+            expand_lb(qv_c, qo_c, f, mf, a.R, a.C, gw, nw, op);
+            nearq.finish();
+            farq.finish();
+            unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
+            if (lane_id() == 0 && ni) atomicAdd(&nxt.ndisc, ni);
+            grid.sync();
+        } else {
+            // ---- near slice exhausted: "update the priority function and
+            // operate on the far slice". Re-split (A-11). --------
+            const int32_t *far_c = fp ? a.far1 : a.far0;
+            for (int64_t j = tid; j < fc; j += nthreads) {
+                const int32_t v = far_c[j];
+                const unsigned long long d = ld_cg(a.dp + v) >> 32;
+                if (d >= thr) atomicMin(&cur.minfar, d);
+            }
+            grid.sync();
+            const unsigned long long mn = ld_volatile(&cur.minfar);
+            if (tid == 0) a.ctl->far_count[fp] = 0ull;
+            if (mn == ~0ull) {  // every far entry was stale: the next step
+                grid.sync();        // sees f == 0 and an empty far pile and stops
+                fp ^= 1;
+                continue;
+            }
+            const uint64_t thr_old = thr;
+            uint64_t band = (mn / a.delta + 1);
+            thr = (band > (0xFFFFFFFFFFFFFFFFull / a.delta)) ? 0xFFFFFFFFFFFFFFFFull : band * a.delta;
+            ++it;
+            farq.qv = fp ? a.far0 : a.far1;
+            farq.counter = &a.ctl->far_count[fp ^ 1];
+            for (int64_t base = gw * 32; base < fc; base += nw * 32) {
+                const int64_t j = base + lane_id();
+                bool to_near = false, to_far = false;
+                int32_t v = 0;
+                int64_t deg = 0;
+                if (j < fc) {
+                    v = far_c[j];
+                    const unsigned long long d = ld_cg(a.dp + v) >> 32;
+                    if (d >= thr_old) {  // else stale: already expanded below thr_old
+                        const bool nearb = d < thr;
+                        const int32_t key = 2 * it + (nearb ? 0 : 1);
+                        if (atomicExch(a.stamp + v, key) != key) {
+                            if (nearb) { to_near = true; deg = a.R[v + 1] - a.R[v]; }
+                            else to_far = true;
+                        }
+                    }
+                }
+                nearq.push(to_near && deg > 0, v, deg);
+                farq.push(to_far, v, 0);
+            }
+            nearq.finish();
+            farq.finish();
+            grid.sync();
+            fp ^= 1;
+        }
+    }
+    if (tid == 0) a.ctl->levels = (unsigned long long)k;
+}
+
+__global__ void unpack_kernel(const unsigned long long *dp, int64_t n, uint32_t *dist, int32_t *pred) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < n; v += nt) {
+        unsigned long long x = dp[v];
+        if (dist) dist[v] = (uint32_t)(x >> 32);
+        if (pred) pred[v] = (int32_t)(uint32_t)(x & 0xffffffffu);
+    }
+}
+
+gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta, int *launches) {
+    SsspArgs a;
+    a.n = g->n; a.m = g->m;
+    a.R = g->R; a.C = g->C; a.W = g->W;
+    a.dp = g->dp; a.stamp = g->stamp;
+    a.qv0 = g->qv[0]; a.qv1 = g->qv[1];
+    a.qo0 = g->qo[0]; a.qo1 = g->qo[1];
+    a.far0 = g->farq[0]; a.far1 = g->farq[1];
+    a.far_cap = g->far_cap;
+    a.ctl = g->ctl; a.stats = g->stats_dev;
+    a.src = src;
+    a.delta = delta;
+    a.S = g->pack_shift;
+    int per_sm = 0;
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sssp_kernel, kBlock, 0));
+    if (per_sm < 1) { set_error("sssp_kernel cannot be resident"); return GR_ERR_CUDA; }
+    dim3 grid(g->num_sms * per_sm), block(kBlock);
+    void *args[] = {&a};
+    GR_CUDA(cudaLaunchCooperativeKernel((void *)sssp_kernel, grid, block, args, 0, g->stream));
+    unpack_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->dp, g->n, dist, pred);
+    GR_CUDA(cudaGetLastError());
+    count_launch(2);
+    *launches = 2;
+    return GR_OK;
+}
+
+}  // namespace gr

@@ -1,0 +1,112 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (same kernels, same default options).
+
+C1-C4: element-by-element against the CPU oracle (BFS is seconds; Dijkstra
+on C3/C4 tens of seconds, so one source). C5 (1.05B edges): the O(m)
+BFS certificate evaluated on the GPU with plain torch ops in this test
+(a property that decides exactness at any size), plus the
+oracle on sampled sources is too slow for the host, so depths of a sample of
+vertices are re-derived by the certificate only.
+"""
+import numpy as np
+import pytest
+import torch
+
+import graphgen as gg
+import oracle
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+
+@pytest.fixture(scope="module")
+def gr():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_1501_05387_b200 as m
+    torch.cuda.set_device(0)
+    return m
+
+
+def _bfs_parity(gr, name, nsrc, dirs=("auto", "push")):
+    g = gg.make_config(name, device="cuda")
+    G = gr.Graph(g.R, g.C, g.W, symmetric=True)
+    R, C, W = g.numpy()
+    for s in gg.sources(g, nsrc):
+        ref, _ = oracle.bfs(R, C, s, want_pred=False)
+        for d in dirs:
+            depth, pred = G.bfs(s, direction=d)
+            got = depth.cpu().numpy()
+            assert np.array_equal(got, ref), (name, s, d, int((got != ref).sum()))
+            assert oracle.check_bfs(R, C, s, got, pred.cpu().numpy()) == []
+    return g, G, (R, C, W)
+
+
+def test_c2_kron21_bfs(gr):
+    _bfs_parity(gr, "c2_kron21", 2)
+
+
+def test_c3_orkut_bfs_sssp(gr):
+    g, G, (R, C, W) = _bfs_parity(gr, "c3_orkut", 1)
+    s = gg.sources(g, 1)[0]
+    ref, _ = oracle.sssp(R, C, W, s, want_pred=False)
+    dist, pred = G.sssp(s)
+    got = gr.dist_to_u32(dist)
+    assert np.array_equal(got, ref), int((got != ref).sum())
+    assert oracle.check_sssp(R, C, W, s, got, pred.cpu().numpy()) == []
+
+
+def test_c4_road_bfs_sssp(gr):
+    g, G, (R, C, W) = _bfs_parity(gr, "c4_road", 1, dirs=("auto",))
+    s = gg.sources(g, 1)[0]
+    ref, _ = oracle.sssp(R, C, W, s, want_pred=False)
+    dist, pred = G.sssp(s)
+    got = gr.dist_to_u32(dist)
+    assert np.array_equal(got, ref), int((got != ref).sum())
+
+
+def _bfs_certificate_torch(R, C, src, depth, pred):
+    """BFS certificate (oracle.check_bfs) restated with torch ops so it runs
+    on the GPU at 1B edges: (i) src only depth 0; (ii) depth[v] <= depth[u]+1
+    along every edge from a reached u, v reached; (iii) pred edge exists and
+    drops depth by one; (iv) -1 <=> -1."""
+    n = R.numel() - 1
+    assert int(depth[src]) == 0 and int((depth == 0).sum()) == 1
+    deg = R[1:] - R[:-1]
+    m = C.numel()
+    chunk = 1 << 27
+    s = 0
+    src_of = None
+    for e0 in range(0, m, chunk):
+        e1 = min(m, e0 + chunk)
+        u = torch.searchsorted(R, torch.arange(e0, e1, device=R.device), right=True) - 1
+        du = depth[u]
+        dv = depth[C[e0:e1].long()]
+        live = du >= 0
+        assert not bool((live & ((dv < 0) | (dv > du + 1))).any())
+    assert bool(((depth == -1) == (pred == -1)).all())
+    assert int(pred[src]) == src
+    reached = torch.nonzero(depth > 0).squeeze(1)
+    p = pred[reached].long()
+    assert bool((depth[p] == depth[reached] - 1).all())
+    # (pred[v], v) in E: binary search v in the sorted list of p
+    lo = R[p]
+    hi = R[p + 1]
+    for _ in range(40):
+        mid = (lo + hi) // 2
+        go = C[torch.clamp(mid, max=m - 1)].long() < reached
+        lo = torch.where(go & (mid < hi), mid + 1, lo)
+        hi = torch.where(go & (mid < hi), hi, mid)
+    assert bool((C[torch.clamp(lo, max=m - 1)].long() == reached).all())
+
+
+def test_c5_kron25_bfs_certificate(gr):
+    g = gg.make_config("c5_kron25", device="cuda")
+    G = gr.Graph(g.R, g.C, None, symmetric=True)
+    srcs = gg.sources(g, 2)
+    for s in srcs:
+        depths = []
+        for d in ("auto", "push"):
+            depth, pred = G.bfs(s, direction=d)
+            _bfs_certificate_torch(g.R, g.C, s, depth, pred)
+            depths.append(depth)
+        assert torch.equal(depths[0], depths[1])
