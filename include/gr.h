@@ -64,7 +64,8 @@ enum {
  *   col_indices  int32[m], each in [0, n). Self-loops and parallel edges are
  *                allowed (BFS ignores them; SSSP takes the minimum weight).
  *   weights      uint32[m] non-negative edge weights w_e, or NULL
- *                for a BFS-only graph.
+ *                for a BFS-only graph (with m = 0 the graph counts as
+ *                weighted: no weight is ever read).
  *   flags        GR_SYMMETRIC | GR_VALIDATE
  *   device       CUDA device ordinal the graph lives on
  *   cuda_stream  cudaStream_t to enqueue all work on (NULL = legacy stream)

@@ -124,7 +124,7 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
     g->stream = (cudaStream_t)stream;
     g->n = n; g->m = m;
     g->symmetric = (flags & GR_SYMMETRIC) != 0;
-    g->has_w = W != nullptr;
+    g->has_w = (W != nullptr) || m == 0;  // m = 0: no weight is ever read
     GR_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, device));
     gr_status st;
 #define TRY(x) do { st = (x); if (st != GR_OK) { dev_free_all(g); delete g; return st; } } while (0)
