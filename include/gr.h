@@ -165,6 +165,7 @@ typedef struct {
     int64_t inspected_edges; /* edges actually read (push: frontier_edges; pull:
                                 up to the first frontier hit, early exit)          */
     int64_t aux;             /* SSSP: far-queue size; BFS: unvisited (heuristic u) */
+    int64_t ns;              /* device time of the step (%globaltimer, ns)         */
 } gr_level_stats;
 
 typedef struct {

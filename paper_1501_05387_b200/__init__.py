@@ -57,7 +57,7 @@ class gr_level_stats(ctypes.Structure):
     _fields_ = [("level", ctypes.c_int32), ("direction", ctypes.c_int32),
                 ("frontier", ctypes.c_int64), ("frontier_edges", ctypes.c_int64),
                 ("discovered", ctypes.c_int64), ("inspected_edges", ctypes.c_int64),
-                ("aux", ctypes.c_int64)]
+                ("aux", ctypes.c_int64), ("ns", ctypes.c_int64)]
 
 
 class gr_run_stats(ctypes.Structure):
@@ -246,7 +246,8 @@ class Graph:
         return dict(num_levels=st.num_levels, delta=st.delta, kernel_launches=st.kernel_launches,
                     levels=[dict(level=r.level, direction=r.direction, frontier=r.frontier,
                                  frontier_edges=r.frontier_edges, discovered=r.discovered,
-                                 inspected_edges=r.inspected_edges, aux=r.aux) for r in recs])
+                                 inspected_edges=r.inspected_edges, aux=r.aux, ns=r.ns)
+                            for r in recs])
 
 
 def dist_to_u32(t):

@@ -9,6 +9,7 @@ LIB = os.path.join(HERE, "libgr_b200.so")
 SOURCES = ["abi.cu", "graph.cu", "bfs.cu", "sssp.cu"]
 HEADERS = ["gr_internal.cuh", "frontier.cuh", os.path.join("..", "..", "include", "gr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+EXTRA = os.environ.get("GR_NVCC_EXTRA", "").split()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
@@ -20,7 +21,10 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, lib=None):
+    global LIB
+    if lib:
+        LIB = lib
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [__file__]
     if not force and not _stale(LIB, deps):
@@ -29,7 +33,7 @@ def build(force=False, verbose=False):
     logs = []
     for s in srcs:
         o = os.path.join(CSRC, os.path.basename(s) + ".o")
-        cmd = [NVCC] + FLAGS + ["-c", s, "-o", o]
+        cmd = [NVCC] + FLAGS + EXTRA + ["-c", s, "-o", o]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs.append(r.stderr)
         if r.returncode != 0:

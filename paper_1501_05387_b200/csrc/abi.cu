@@ -4,6 +4,7 @@
 // of bfs.cu / sssp.cu.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include <atomic>
 
@@ -28,6 +29,11 @@ gr_status cuda_fail(cudaError_t e, const char *what, const char *file, int line)
 }
 
 void count_launch(int k) { g_launches.fetch_add((unsigned long long)k); }
+
+int64_t env_int(const char *name, int64_t dflt) {
+    const char *v = getenv(name);
+    return (v && *v) ? atoll(v) : dflt;
+}
 
 gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C, const uint32_t *W,
                        uint32_t flags, int device, void *stream, Graph **out);
@@ -69,6 +75,7 @@ const char *gr_last_error(void) { return g_err; }
 uint64_t gr_kernel_launch_count(void) { return g_launches.load(); }
 
 const char *gr_version(void) { return "gr_b200 0.1 sm_100a"; }
+
 
 gr_status gr_graph_create(int64_t n, int64_t m, const int64_t *row_offsets, const int32_t *col_indices,
                           const uint32_t *weights, uint32_t flags, int device, void *cuda_stream,

@@ -5,9 +5,30 @@
 // Paper: BFS §5.1; advance/filter; fusion;
 // load balancing; idempotent vs atomic discovery (P:793-802,
 // P:916-921); push vs pull. Readings A-1..A-6 in DESIGN.md.
+//
+// Level modes:
+//  * grid push  -- merge-path advance over the global queue, every warp of the
+//                  grid (expand_lb + BfsPushOp); also sets the next frontier's
+//                  bits in a rotating frontier bitmap so a following pull
+//                  level needs no conversion;
+//  * grid pull  -- bottom-up sweep over the frontier bitmap (pull_level);
+//  * small push -- frontier <= kSmallF vertices and <= kSmallE edges: CTA 0
+//                  alone runs consecutive levels with the frontier queue in
+//                  SHARED memory and CTA barriers (tiny levels are pure
+//                  latency: a grid barrier and L2 round trips per control
+//                  word would dominate).
+// Control words every block needs (frontier size, counters) are read by one
+// thread per CTA and broadcast through shared memory: thousands of warps
+// reading one L2 address serialise on its slice.
 #include "frontier.cuh"
 
 namespace gr {
+
+constexpr int64_t kSmallF = 4096;   // small mode: queue capacity (shared memory)
+constexpr int64_t kSmallFDefault = 1024;  // small mode: default max frontier (swept on C4)
+constexpr int64_t kSmallE = 16384;  // small mode: max frontier edges
+constexpr int kSmallCntBits = 24;   // count field of the small-mode packed counter
+constexpr unsigned long long kSmallCntMask = (1ull << kSmallCntBits) - 1;
 
 struct BfsArgs {
     int64_t n, m;
@@ -16,9 +37,10 @@ struct BfsArgs {
     const int64_t *Rt;   // in-edges for pull (== R when symmetric)
     const int32_t *Ct;
     uint32_t *visited;
-    uint32_t *fbuf0, *fbuf1;
-    int32_t *qv0, *qv1;
-    int64_t *qo0, *qo1;
+    const uint32_t *noin;  // vertices with in-degree 0
+    uint32_t *fbuf[3];     // rotating frontier bitmaps
+    int32_t *qv[2];
+    int64_t *qo[2];
     int32_t *depth;
     int32_t *pred;       // may be null
     Ctl *ctl;
@@ -30,9 +52,31 @@ struct BfsArgs {
     double alpha, beta;
     int64_t nonisolated;
     int S;
+    int64_t small_f, small_e;  // small-mode thresholds (<= kSmallF, tuning knobs)
 };
 
-// Per-edge op of the push advance: the fused cond/apply + filter of BFS.
+struct BfsSmem {
+    union {
+        struct {  // grid levels: per-warp append staging
+            int32_t sv[kWarpsPerBlock][kStageCap];
+            int32_t sd[kWarpsPerBlock][kStageCap];
+        } stage;
+        struct {  // small mode: the frontier lives here (double-buffered)
+            int64_t rs[2][kSmallF];   // row start of each entry
+            int64_t off[2][kSmallF];  // exclusive degree prefix (reserved at append time)
+            int32_t q[2][kSmallF];    // vertex ids
+        } small;
+    } u;
+    unsigned long long ctl[8];
+    long long scan[kWarpsPerBlock];
+    unsigned long long bsum[4];
+    unsigned long long pk[3];   // small mode: packed (edges << kSmallCntBits) | count, per level mod 3
+    unsigned long long nd[3];   // small mode: discovered per level mod 3
+    int work;
+};
+
+// ---------------------------------------------------------------------------
+// Per-edge op of the grid push advance: the fused cond/apply + filter of BFS.
 // cond: "is d unvisited" (bitmap probe, culling heuristic P:797-799);
 // claim: atomicOr on the visited word returns the old bit, so each vertex is
 // discovered exactly once ("non-idempotent advance ... uses atomic
@@ -42,8 +86,10 @@ struct BfsArgs {
 // authoritative visited test, plain stores write it, the bitmap is updated
 // with a fire-and-forget red.or and only filters (reading A-6); duplicates may
 // enter the queue and are harmless (same depth).
+// ---------------------------------------------------------------------------
 struct BfsPushOp {
     uint32_t *visited;
+    uint32_t *fbn;       // next frontier bitmap (null: not maintained this level)
     int32_t *depth;
     int32_t *pred;
     const int64_t *R;
@@ -51,6 +97,9 @@ struct BfsPushOp {
     int32_t idempotent;
     Appender *app;
     unsigned long long ndisc;
+    unsigned long long pol_keep;   // evict_last policy for the visited bitmap
+    bool probe;          // culling probe before the claim (big levels); small levels
+                         // claim directly: one L2 round trip less on the critical path
 
     __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
 
@@ -59,38 +108,117 @@ struct BfsPushOp {
                                           const int32_t *dst, const int64_t *) {
         uint32_t word[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) word[u] = ok[u] ? ld_cg(visited + (dst[u] >> 5)) : 0xffffffffu;
+        for (int u = 0; u < U; ++u)
+            word[u] = (ok[u] && probe) ? ld_probe(visited + (dst[u] >> 5), pol_keep)
+                                       : (ok[u] ? 0u : 0xffffffffu);
+        bool disc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            int32_t w = dst[u];
-            uint32_t bit = 1u << (w & 31);
-            bool disc = false;
-            int64_t deg = 0;
+            const int32_t w = dst[u];
+            const uint32_t bit = 1u << (w & 31);
+            disc[u] = false;
             if (ok[u] && !(word[u] & bit)) {
                 if (idempotent) {
                     if (*(volatile int32_t *)(depth + w) < 0) {
-                        disc = true;
-                        depth[w] = next_depth;
+                        disc[u] = true;
                         atomicOr(visited + (w >> 5), bit);  // result unused -> RED.OR
                     }
                 } else {
-                    uint32_t old = atomicOr(visited + (w >> 5), bit);
-                    if (!(old & bit)) {
-                        disc = true;
-                        depth[w] = next_depth;
-                    }
-                }
-                if (disc) {
-                    if (pred) pred[w] = src[u];
-                    deg = R[w + 1] - R[w];
+                    const uint32_t old = atomicOr(visited + (w >> 5), bit);
+                    disc[u] = !(old & bit);
                 }
             }
-            ndisc += disc;
-            app->push(disc && deg > 0, w, deg);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (!__any_sync(0xffffffffu, disc[u])) continue;
+            const int32_t w = dst[u];
+            int64_t deg = 0;
+            if (disc[u]) {
+                depth[w] = next_depth;
+                if (pred) pred[w] = src[u];
+                if (fbn) atomicOr(fbn + (w >> 5), 1u << (w & 31));  // RED.OR
+                deg = R[w + 1] - R[w];
+                ++ndisc;
+            }
+            app->push(disc[u] && deg > 0, w, deg);
         }
     }
 };
 
+// Small-mode op: claim directly with atomicOr (one L2 round trip instead of
+// probe + claim) while the target's row offsets are loaded speculatively in
+// parallel, then append (vertex, row start, degree) into the shared-memory
+// queue of the next level and prefetch the head of its neighbour list into L2
+// (the next level reads it a few microseconds later). Entries beyond kSmallF
+// spill to the global queue, which then ends small mode.
+struct SmallPushOp {
+    uint32_t *visited;
+    int32_t *depth;
+    int32_t *pred;
+    const int64_t *R;
+    const int32_t *C;
+    int32_t next_depth;
+    int32_t *sq_next;            // smem vertex ids
+    int64_t *srs_next;           // smem row starts
+    int64_t *soff_next;          // smem degree prefix
+    unsigned long long *spk;     // smem packed counter (edges << kSmallCntBits) | count
+    int32_t *gq_next;            // global spill queue (entries >= kSmallF)
+    int64_t *go_next;
+    unsigned long long ndisc;
+
+    __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
+
+    template <int U>
+    __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *,
+                                          const int32_t *dst, const int64_t *) {
+        uint32_t old[U];
+        int64_t rs[U], re[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            old[u] = ok[u] ? atomicOr(visited + (dst[u] >> 5), 1u << (dst[u] & 31)) : 0xffffffffu;
+            rs[u] = ok[u] ? R[dst[u]] : 0;
+            re[u] = ok[u] ? R[dst[u] + 1] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t w = dst[u];
+            const bool disc = !((old[u] >> (w & 31)) & 1u);
+            const unsigned mask = __ballot_sync(0xffffffffu, disc);
+            if (!mask) continue;
+            // one packed shared-memory atomic reserves the queue slots AND the
+            // edge range: the next level's degree prefix comes out of the append
+            const int64_t deg = disc ? re[u] - rs[u] : 0;
+            const int64_t incl = warp_incl_scan<int64_t>(deg);
+            const int64_t tot = __shfl_sync(0xffffffffu, incl, 31);
+            unsigned long long base = 0;
+            if (lane_id() == 0)
+                base = atomicAdd(spk, ((unsigned long long)tot << kSmallCntBits) | (unsigned long long)__popc(mask));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (disc) {
+                depth[w] = next_depth;
+                if (pred) pred[w] = src[u];
+                const int64_t pos = (int64_t)(base & kSmallCntMask) + __popc(mask & lanemask_lt());
+                const int64_t off = (int64_t)(base >> kSmallCntBits) + incl - deg;
+                if (pos < kSmallF) {
+                    sq_next[pos] = w;
+                    srs_next[pos] = rs[u];
+                    soff_next[pos] = off;
+                } else {
+                    gq_next[pos] = w;
+                    go_next[pos] = off;
+                }
+                if (deg > 0) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs[u]));
+                    if (deg > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs[u] + 32));
+                }
+                ++ndisc;
+            }
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
 // Pull (bottom-up) step over in-edges: "pull starts with a
 // frontier of unvisited vertices, generating the new frontier by filtering
 // the unvisited frontier for vertices that have neighbors in the current
@@ -98,26 +226,40 @@ struct BfsPushOp {
 // owns 32 consecutive vertices = one bitmap word, so the next-frontier word
 // and the visited word are written with one plain store from a ballot: no
 // atomics. Each lane stops at its first in-neighbour in the frontier (early
-// exit).
+// exit). Each CTA owns a contiguous range of words; its warps take words from
+// a shared-memory counter (per-vertex scan lengths vary widely).
+// ---------------------------------------------------------------------------
 __device__ __forceinline__ void pull_level(const BfsArgs &a, const uint32_t *__restrict__ fcur,
                                            uint32_t *__restrict__ fnext, int32_t next_depth,
-                                           int64_t gw, int64_t nw, Appender &app,
-                                           unsigned long long &ndisc, unsigned long long &insp) {
+                                           int *swork, Appender &app, unsigned long long &ndisc,
+                                           unsigned long long &insp) {
     const int64_t nwords = (a.n + 31) / 32;
+    const int64_t wb0 = nwords * blockIdx.x / gridDim.x;
+    const int64_t wb1 = nwords * (blockIdx.x + 1) / gridDim.x;
     const unsigned l = lane_id();
-    for (int64_t wi = gw; wi < nwords; wi += nw) {
-        int64_t v = wi * 32 + l;
-        uint32_t visw = a.visited[wi];
-        bool cand = v < a.n && !((visw >> l) & 1u);
+    const unsigned long long pol = policy_evict_first();
+    for (;;) {
+        int c = 0;
+        if (l == 0) c = atomicAdd(swork, 1);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const int64_t wi = wb0 + c;
+        if (wi >= wb1) break;
+        const int64_t v = wi * 32 + l;
+        const uint32_t visw = a.visited[wi];
+        if (visw == 0xffffffffu) {  // every vertex of the word already visited
+            if (l == 0) fnext[wi] = 0u;
+            continue;
+        }
+        const bool cand = v < a.n && !((visw >> l) & 1u);
         bool found = false;
         int32_t parent = -1;
         if (cand) {
-            int64_t beg = a.Rt[v], end = a.Rt[v + 1];
+            const int64_t beg = a.Rt[v], end = a.Rt[v + 1];
             for (int64_t e = beg; e < end && !found; e += 4) {
                 int32_t u[4];
                 uint32_t fw[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) u[k] = (e + k < end) ? __ldg(a.Ct + e + k) : -1;
+                for (int k = 0; k < 4; ++k) u[k] = (e + k < end) ? ld_stream(a.Ct + e + k, pol) : -1;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) fw[k] = (u[k] >= 0) ? __ldg(fcur + (u[k] >> 5)) : 0u;
 #pragma unroll
@@ -132,11 +274,12 @@ __device__ __forceinline__ void pull_level(const BfsArgs &a, const uint32_t *__r
                 }
             }
         }
-        unsigned nb = __ballot_sync(0xffffffffu, found);
+        const unsigned nb = __ballot_sync(0xffffffffu, found);
         if (l == 0) {
             fnext[wi] = nb;
             if (nb) a.visited[wi] = visw | nb;
         }
+        if (nb == 0) continue;
         int64_t deg = 0;
         if (found) {
             a.depth[v] = next_depth;
@@ -148,10 +291,61 @@ __device__ __forceinline__ void pull_level(const BfsArgs &a, const uint32_t *__r
     }
 }
 
-__global__ void __launch_bounds__(kBlock) bfs_kernel(BfsArgs a) {
+// Direction decision (reading A-3). Pure function of counters
+// every block reads after the same barrier, so all blocks agree.
+__device__ __forceinline__ int decide_direction(const BfsArgs &a, int dir, int64_t f, int64_t mf,
+                                                int64_t u_cnt, int64_t m_u, int64_t prev_f,
+                                                int64_t nwords) {
+    if (a.direction != 0) return a.direction;
+    if (a.switch_rule == 1) return (u_cnt < f) ? 2 : 1;  // paper-literal: unvisited < frontier
+    if (dir == 1) {
+        // Beamer: pull when the frontier's edges exceed the unvisited edges / alpha;
+        // plus: a pull step sweeps every bitmap word, so require m_f >= n/32.
+        if ((double)mf > (double)m_u / a.alpha && mf >= nwords) return 2;
+        return 1;
+    }
+    if ((double)f < (double)a.nonisolated / a.beta && f < prev_f) return 1;
+    return 2;
+}
+
+struct BfsState {  // per-traversal heuristic state, identical in every CTA
+    int L;
+    int dir, prev_dir;
+    int64_t u_cnt, m_u, prev_f;
+    int fb_valid;       // fbuf[L%3] holds the frontier of level L
+    int fbn_clean;      // fbuf[(L+1)%3] is all zero
+    int closed;         // stats records below this level are closed
+};
+
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Block-wide exclusive scan of one int64 per thread; returns the exclusive
+// prefix, total in *total. Uses s->scan; contains two __syncthreads.
+__device__ __forceinline__ int64_t block_excl_scan(int64_t x, int64_t *total, BfsSmem *s) {
+    const int wib = threadIdx.x >> 5;
+    const int64_t incl = warp_incl_scan<int64_t>(x);
+    __syncthreads();  // s->scan / s->bsum[3] may still be read by a previous scan
+    if (lane_id() == 31) s->scan[wib] = incl;
+    __syncthreads();
+    if (wib == 0) {
+        const int64_t y = (lane_id() < kWarpsPerBlock) ? s->scan[lane_id()] : 0;
+        const int64_t yi = warp_incl_scan<int64_t>(y);
+        if (lane_id() < kWarpsPerBlock) s->scan[lane_id()] = yi - y;
+        if (lane_id() == 31) s->bsum[3] = (unsigned long long)yi;
+    }
+    __syncthreads();
+    *total = (int64_t)s->bsum[3];
+    return s->scan[wib] + incl - x;
+}
+
+__global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ int32_t s_v[kWarpsPerBlock][kStageCap];
-    __shared__ int64_t s_d[kWarpsPerBlock][kStageCap];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BfsSmem *s = reinterpret_cast<BfsSmem *>(smem_raw);
 
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -166,7 +360,9 @@ __global__ void __launch_bounds__(kBlock) bfs_kernel(BfsArgs a) {
         a.depth[v] = -1;
         if (a.pred) a.pred[v] = -1;
     }
-    for (int64_t w = tid; w < nwords; w += nthreads) a.visited[w] = 0u;
+    // vertices with no in-edge can never be discovered: pre-mark them visited
+    // so pull skips them (they keep depth -1; the bitmap is internal)
+    for (int64_t w = tid; w < nwords; w += nthreads) a.visited[w] = a.noin[w];
     if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) ((unsigned long long *)a.ctl->slot)[tid] = 0ull;
     if (tid == 0) a.ctl->overflow = 0ull;
     grid.sync();
@@ -174,112 +370,263 @@ __global__ void __launch_bounds__(kBlock) bfs_kernel(BfsArgs a) {
     if (tid == 0) {
         a.depth[a.src] = 0;
         if (a.pred) a.pred[a.src] = a.src;  // A-1
-        a.visited[a.src >> 5] = 1u << (a.src & 31);
-        if (deg_src > 0) {
-            a.qv0[0] = a.src;
-            a.qo0[0] = 0;
-            a.ctl->slot[0].qpack = ((unsigned long long)deg_src << a.S) | 1ull;
-        }
+        a.visited[a.src >> 5] |= 1u << (a.src & 31);
+        a.qv[0][0] = a.src;
+        a.qo[0][0] = 0;
+        a.ctl->slot[0].qpack = (deg_src > 0) ? (((unsigned long long)deg_src << a.S) | 1ull) : 0ull;
     }
     grid.sync();
 
-    // Heuristic state (identical in every block: computed from the same
-    // counters after each grid barrier). u = unvisited non-isolated vertices,
-    // m_u = edges incident to them (reading A-3).
-    int64_t u_cnt = a.nonisolated - 1;
-    int64_t m_u = a.m - deg_src;
-    int dir = (a.direction == 2) ? 2 : 1;
-    int prev_dir = 1;  // the initial frontier is a queue
-    int64_t prev_f = 0;
+    // Heuristic state. u = unvisited vertices that have an in-edge, m_u =
+    // edges incident to them (reading A-3).
+    const bool src_has_in = !((a.noin[a.src >> 5] >> (a.src & 31)) & 1u);
+    BfsState st;
+    st.L = 0;
+    st.dir = (a.direction == 2) ? 2 : 1;
+    st.prev_dir = 1;
+    st.u_cnt = a.nonisolated - (src_has_in ? 1 : 0);
+    st.m_u = a.m - deg_src;
+    st.prev_f = 0;
+    st.fb_valid = 0;
+    st.fbn_clean = 0;
+    st.closed = 0;
+    const unsigned long long pol_keep = policy_evict_last();
+    long long t_prev = 0;
+    if (tid == 0) t_prev = gtimer();
+    bool pending = false;  // counters of the last grid level not yet applied to u, m_u
 
     Appender app;
-    app.sv = s_v[wib];
-    app.sd = s_d[wib];
+    app.sv = s->u.stage.sv[wib];
+    app.sd = s->u.stage.sd[wib];
     app.cnt = 0;
     app.S = a.S;
     app.cap = a.n;
     app.overflow = &a.ctl->overflow;
 
-    int L = 0;
-    for (;; ++L) {
-        Slot &cur = a.ctl->slot[L & 3];
-        Slot &nxt = a.ctl->slot[(L + 1) & 3];
-        const unsigned long long qp = ld_volatile(&cur.qpack);
+    for (;;) {
+        // ---- control words of level L: one thread reads, the CTA shares ----
+        const int L = st.L;
+        if (threadIdx.x == 0) {
+            const Slot &cur = a.ctl->slot[L & 3];
+            // independent relaxed loads: issued back to back, one round trip
+            const unsigned long long q0 = ld_relaxed(&cur.qpack), q1 = ld_relaxed(&cur.ndisc),
+                                     q2 = ld_relaxed(&cur.insp), q3 = ld_relaxed(&a.ctl->overflow);
+            s->ctl[0] = q0; s->ctl[1] = q1; s->ctl[2] = q2; s->ctl[3] = q3;
+        }
+        __syncthreads();
+        const unsigned long long qp = s->ctl[0];
         const int64_t f = (int64_t)(qp & cmask);
         const int64_t mf = (int64_t)(qp >> a.S);
-        if (L > 0 && tid == 0 && L - 1 < kMaxStatRecords) {
-            gr_level_stats &st = a.stats[L - 1];
-            st.discovered = (int64_t)ld_volatile(&cur.ndisc);
-            if (st.direction == 2) st.inspected_edges = (int64_t)ld_volatile(&cur.insp);
+        if (pending) {
+            st.u_cnt -= (int64_t)s->ctl[1];
+            st.m_u -= mf;
+            pending = false;
         }
-        if (f == 0 || ld_volatile(&a.ctl->overflow)) break;
+        if (tid == 0 && L > st.closed && L - 1 < kMaxStatRecords) {
+            gr_level_stats &sr = a.stats[L - 1];
+            sr.discovered = (int64_t)s->ctl[1];
+            if (sr.direction == 2) sr.inspected_edges = (int64_t)s->ctl[2];
+            const long long t = gtimer();
+            sr.ns = t - t_prev;
+            t_prev = t;
+        }
+        const bool stop = (f == 0 || s->ctl[3]);
+        __syncthreads();  // s->ctl is rewritten below
+        if (stop) break;
+        const int dir = decide_direction(a, st.dir, f, mf, st.u_cnt, st.m_u, st.prev_f, nwords);
 
-        // ---- direction decision (reading A-3) -------------------
-        if (a.direction == 0) {
-            if (a.switch_rule == 1) {
-                dir = (u_cnt < f) ? 2 : 1;  // paper-literal: unvisited < frontier
-            } else if (dir == 1) {
-                if ((double)mf > (double)m_u / a.alpha) dir = 2;
-            } else {
-                if ((double)f < (double)a.nonisolated / a.beta && f < prev_f) dir = 1;
+        if (dir == 1 && f <= a.small_f && mf <= a.small_e) {
+            // ================= small mode: CTA 0 alone ===========================
+            if (blockIdx.x == 0) {
+                int c = 0, r = 0;
+                for (int64_t j = threadIdx.x; j < f; j += kBlock) {
+                    const int32_t v = a.qv[L & 1][j];
+                    s->u.small.q[0][j] = v;
+                    s->u.small.off[0][j] = a.qo[L & 1][j];
+                    s->u.small.rs[0][j] = a.R[v];
+                }
+                if (threadIdx.x < 3) { s->pk[threadIdx.x] = 0; s->nd[threadIdx.x] = 0; }
+                __syncthreads();
+                int64_t cf = f, E = mf;
+                bool mu_pending = false;
+                bool done = false;
+                long long tp = t_prev;
+                for (;;) {
+                    if (cf > a.small_f) break;  // too large (or spilled to the global queue)
+#ifdef GR_TRACE
+                    if (threadIdx.x == 0) g_trace_L = st.L;
+#endif
+                    GR_TSTAMP(0);
+                    if (mu_pending) { st.m_u -= E; mu_pending = false; }
+                    if (cf == 0) { done = true; break; }
+                    const int d = decide_direction(a, st.dir, cf, E, st.u_cnt, st.m_u, st.prev_f, nwords);
+                    if (!(d == 1 && E <= a.small_e)) break;
+                    st.dir = d;
+                    const int Lc = st.L;
+                    const int r1 = (r + 1) % 3, r2 = (r + 2) % 3;
+                    if (threadIdx.x == 0) {
+                        s->pk[r2] = 0;  // counter of level Lc + 2 (last read at level Lc - 1)
+                        s->nd[r2] = 0;
+                        if (Lc < kMaxStatRecords) {
+                            gr_level_stats &sr = a.stats[Lc];
+                            sr.level = Lc; sr.direction = 1; sr.frontier = cf; sr.frontier_edges = E;
+                            sr.discovered = 0; sr.inspected_edges = E; sr.aux = st.u_cnt; sr.ns = 0;
+                        }
+                    }
+                    SmallPushOp op{a.visited, a.depth, a.pred, a.R, a.C, Lc + 1, s->u.small.q[c ^ 1],
+                                   s->u.small.rs[c ^ 1], s->u.small.off[c ^ 1], &s->pk[r1],
+                                   a.qv[(Lc + 1) & 1], a.qo[(Lc + 1) & 1], 0ull};
+                    SmemFrontier fr{s->u.small.q[c], s->u.small.off[c], s->u.small.rs[c], cf, E};
+                    GR_TSTAMP(9);
+                    expand_lb(fr, a.C, (int64_t)wib, (int64_t)kWarpsPerBlock, op);
+                    GR_TSTAMP(5);
+                    const unsigned long long ndw = warp_sum<unsigned long long>(op.ndisc);
+                    if (lane_id() == 0 && ndw) atomicAdd(&s->nd[r1], ndw);
+                    __syncthreads();
+                    const unsigned long long pk = s->pk[r1];
+                    const unsigned long long ndl = s->nd[r1];
+                    GR_TSTAMP(6);
+                    if (threadIdx.x == 0 && Lc < kMaxStatRecords) {
+                        const long long t = gtimer();
+                        a.stats[Lc].discovered = (int64_t)ndl;
+                        a.stats[Lc].ns = t - tp;
+                        tp = t;
+                    }
+                    st.u_cnt -= (int64_t)ndl;
+                    st.prev_f = cf;
+                    st.prev_dir = 1;
+                    st.L = Lc + 1;
+                    c ^= 1;
+                    r = r1;
+                    cf = (int64_t)(pk & kSmallCntMask);
+                    E = (int64_t)(pk >> kSmallCntBits);
+                    mu_pending = true;
+                }
+                // hand the frontier of level st.L back to the grid
+                if (!done) {
+                    // the frontier of level st.L: entries below kSmallF are in shared
+                    // memory, the rest were spilled (with their offsets) to the global queue
+                    for (int64_t j = threadIdx.x; j < cf && j < kSmallF; j += kBlock) {
+                        a.qv[st.L & 1][j] = s->u.small.q[c][j];
+                        a.qo[st.L & 1][j] = s->u.small.off[c][j];
+                    }
+                    if (mu_pending) st.m_u -= E;
+                    if (threadIdx.x == 0) {
+                        a.ctl->slot[st.L & 3].qpack = ((unsigned long long)E << a.S) | (unsigned long long)cf;
+                        a.ctl->slot[st.L & 3].ndisc = 0;
+                        a.ctl->slot[st.L & 3].insp = 0;
+                    }
+                } else if (threadIdx.x == 0) {
+                    a.ctl->slot[st.L & 3].qpack = 0;
+                }
+                if (threadIdx.x == 0) {
+                    for (int k = 1; k <= 2; ++k) {
+                        Slot &r = a.ctl->slot[(st.L + k) & 3];
+                        r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull;
+                    }
+                    long long *bs = a.ctl->bstate;
+                    bs[0] = st.L; bs[1] = st.dir; bs[2] = st.prev_dir; bs[3] = st.u_cnt;
+                    bs[4] = st.m_u; bs[5] = st.prev_f; bs[6] = tp;
+                }
             }
+            grid.sync();
+            if (threadIdx.x == 0) {
+                const volatile long long *bs = a.ctl->bstate;
+                for (int k = 0; k < 7; ++k) s->ctl[k] = (unsigned long long)bs[k];
+            }
+            __syncthreads();
+            st.L = (int)(long long)s->ctl[0];
+            st.dir = (int)(long long)s->ctl[1];
+            st.prev_dir = (int)(long long)s->ctl[2];
+            st.u_cnt = (long long)s->ctl[3];
+            st.m_u = (long long)s->ctl[4];
+            st.prev_f = (long long)s->ctl[5];
+            if (tid == 0) t_prev = (long long)s->ctl[6];
+            st.closed = st.L;      // records below st.L are closed
+            st.fb_valid = 0;       // small mode keeps no frontier bitmap
+            st.fbn_clean = 0;
+            pending = false;
+            __syncthreads();
+            continue;
         }
+
+        // ===================== grid level ======================================
+#ifdef GR_TRACE
+        if (tid == 0) g_trace_L = L;
+#endif
+        GR_TSTAMP(0);
+        st.dir = dir;
         if (tid == 0) {
             Slot &rst = a.ctl->slot[(L + 2) & 3];
-            rst.qpack = 0; rst.ndisc = 0; rst.fpack = 0; rst.work = 0; rst.minfar = ~0ull;
-            rst.insp = 0;
+            rst.qpack = 0; rst.ndisc = 0; rst.fpack = 0; rst.work = 0; rst.minfar = ~0ull; rst.insp = 0;
             if (L < kMaxStatRecords) {
-                gr_level_stats &st = a.stats[L];
-                st.level = L; st.direction = dir; st.frontier = f; st.frontier_edges = mf;
-                st.discovered = 0; st.inspected_edges = (dir == 1) ? mf : 0; st.aux = u_cnt;
+                gr_level_stats &sr = a.stats[L];
+                sr.level = L; sr.direction = dir; sr.frontier = f; sr.frontier_edges = mf;
+                sr.discovered = 0; sr.inspected_edges = (dir == 1) ? mf : 0; sr.aux = st.u_cnt; sr.ns = 0;
             }
         }
-
-        int32_t *qv_c = (L & 1) ? a.qv1 : a.qv0;
-        int64_t *qo_c = (L & 1) ? a.qo1 : a.qo0;
-        int32_t *qv_n = (L & 1) ? a.qv0 : a.qv1;
-        int64_t *qo_n = (L & 1) ? a.qo0 : a.qo1;
-        uint32_t *fb_c = (L & 1) ? a.fbuf1 : a.fbuf0;
-        uint32_t *fb_n = (L & 1) ? a.fbuf0 : a.fbuf1;
-
-        app.qv = qv_n;
-        app.qo = qo_n;
+        if (threadIdx.x == 0) { s->work = 0; s->bsum[0] = 0; s->bsum[1] = 0; }
+        Slot &nxt = a.ctl->slot[(L + 1) & 3];
+        app.qv = a.qv[(L + 1) & 1];
+        app.qo = a.qo[(L + 1) & 1];
         app.counter = &nxt.qpack;
-        unsigned long long ndisc = 0;
-
-        if (dir == 1) {
-            BfsPushOp op{a.visited, a.depth, a.pred, a.R, L + 1, a.idempotent, &app, 0ull};
-            expand_lb(qv_c, qo_c, f, mf, a.R, a.C, gw, nw, op);
-            ndisc = op.ndisc;
-        } else {
-            if (prev_dir == 1) {
-                // queue -> bitmap conversion ("converts the current
-                // frontier into a bitmap of vertices")
-                for (int64_t w = tid; w < nwords; w += nthreads) fb_c[w] = 0u;
-                grid.sync();
-                for (int64_t j = tid; j < f; j += nthreads) {
-                    int32_t v = qv_c[j];
-                    atomicOr(fb_c + (v >> 5), 1u << (v & 31));
-                }
-                grid.sync();
+        uint32_t *fb_c = a.fbuf[L % 3];
+        uint32_t *fb_n = a.fbuf[(L + 1) % 3];
+        uint32_t *fb_z = a.fbuf[(L + 2) % 3];
+        unsigned long long ndisc = 0, insp = 0;
+        if (dir == 2 && !st.fb_valid) {
+            // queue -> bitmap conversion ("converts the current
+            // frontier into a bitmap of vertices")
+            for (int64_t w = tid; w < nwords; w += nthreads) fb_c[w] = 0u;
+            grid.sync();
+            const int32_t *qv_c = a.qv[L & 1];
+            for (int64_t j = tid; j < f; j += nthreads) {
+                const int32_t v = qv_c[j];
+                atomicOr(fb_c + (v >> 5), 1u << (v & 31));
             }
-            unsigned long long insp = 0;
-            pull_level(a, fb_c, fb_n, L + 1, gw, nw, app, ndisc, insp);
-            insp = warp_sum<unsigned long long>(insp);
-            if (lane_id() == 0 && insp) atomicAdd(&nxt.insp, insp);
+            grid.sync();
         }
+        // clear the bitmap level L+1 will fill (it was last read at level L-1);
+        // only when a pull level is plausible soon: a sweep over n/32 words is
+        // not free on high-diameter graphs with thousands of tiny levels
+        const bool need_fb = (dir == 2) || (mf >= nwords / 4);
+        if (need_fb)
+            for (int64_t w = tid; w < nwords; w += nthreads) fb_z[w] = 0u;
+        if (dir == 1) {
+            BfsPushOp op{a.visited, st.fbn_clean ? fb_n : nullptr, a.depth, a.pred, a.R, L + 1,
+                         a.idempotent, &app, 0ull, pol_keep, mf >= (1 << 16)};
+            GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.R, f, mf};
+            expand_lb(fr, a.C, gw, nw, op);
+            ndisc = op.ndisc;
+            st.fb_valid = st.fbn_clean;
+        } else {
+            pull_level(a, fb_c, fb_n, L + 1, &s->work, app, ndisc, insp);
+            st.fb_valid = 1;
+        }
+        GR_TSTAMP(5);
         app.finish();
+        GR_TSTAMP(6);
         ndisc = warp_sum<unsigned long long>(ndisc);
-        if (lane_id() == 0 && ndisc) atomicAdd(&nxt.ndisc, ndisc);
-        prev_dir = dir;
-        prev_f = f;
+        insp = warp_sum<unsigned long long>(insp);
+        if (lane_id() == 0) {
+            if (ndisc) atomicAdd(&s->bsum[0], ndisc);
+            if (insp) atomicAdd(&s->bsum[1], insp);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            if (s->bsum[0]) atomicAdd(&nxt.ndisc, s->bsum[0]);
+            if (s->bsum[1]) atomicAdd(&nxt.insp, s->bsum[1]);
+        }
+        st.prev_dir = dir;
+        st.prev_f = f;
+        st.fbn_clean = need_fb;
+        st.L = L + 1;
+        pending = true;
+        GR_TSTAMP(7);
         grid.sync();
-        const unsigned long long nq = ld_volatile(&nxt.qpack);
-        const unsigned long long nd = ld_volatile(&nxt.ndisc);
-        u_cnt -= (int64_t)nd;
-        m_u -= (int64_t)(nq >> a.S);
+        GR_TSTAMP(8);
     }
-    if (tid == 0) a.ctl->levels = (unsigned long long)L;
+    if (tid == 0) a.ctl->levels = (unsigned long long)st.L;
 }
 
 gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr_bfs_opts &o,
@@ -288,9 +635,9 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.n = g->n; a.m = g->m;
     a.R = g->R; a.C = g->C; a.Rt = g->Rt; a.Ct = g->Ct;
     a.visited = g->visited;
-    a.fbuf0 = g->fbuf[0]; a.fbuf1 = g->fbuf[1];
-    a.qv0 = g->qv[0]; a.qv1 = g->qv[1];
-    a.qo0 = g->qo[0]; a.qo1 = g->qo[1];
+    a.noin = g->noin;
+    for (int i = 0; i < 3; ++i) a.fbuf[i] = g->fbuf[i];
+    for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; }
     a.depth = depth; a.pred = pred;
     a.ctl = g->ctl; a.stats = g->stats_dev;
     a.src = src;
@@ -301,16 +648,30 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.beta = o.beta > 0 ? o.beta : 24.0;
     a.nonisolated = g->nonisolated;
     a.S = g->pack_shift;
+    a.small_f = env_int("GR_SMALL_F", kSmallFDefault);
+    a.small_e = env_int("GR_SMALL_E", kSmallE);
+    if (a.small_f > kSmallF) a.small_f = kSmallF;
 
-    int per_sm = 0;
-    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, kBlock, 0));
+    static int per_sm = 0;  // occupancy of the kernel (same on every device of the box)
+    const size_t smem = sizeof(BfsSmem);
+    if (per_sm == 0) {
+        GR_CUDA(cudaFuncSetAttribute(bfs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, kBlock, smem));
+    }
     if (per_sm < 1) { set_error("bfs_kernel cannot be resident"); return GR_ERR_CUDA; }
     dim3 grid(g->num_sms * per_sm), block(kBlock);
     void *args[] = {&a};
-    GR_CUDA(cudaLaunchCooperativeKernel((void *)bfs_kernel, grid, block, args, 0, g->stream));
+    GR_CUDA(cudaLaunchCooperativeKernel((void *)bfs_kernel, grid, block, args, smem, g->stream));
     count_launch();
     *launches = 1;
     return GR_OK;
 }
 
 }  // namespace gr
+
+#ifdef GR_TRACE
+// debug only (not in gr.h): install the BFS level trace buffer (16 stamps x 256 levels)
+extern "C" int gr_debug_trace_set(long long *dev_buf) {
+    return (int)cudaMemcpyToSymbol(gr::g_trace, &dev_buf, sizeof(dev_buf));
+}
+#endif

@@ -26,14 +26,34 @@
 
 namespace gr {
 
+// Debug trace (GR_TRACE builds only): thread 0 stamps %globaltimer at fixed
+// points of the first levels; read back with gr_debug_trace().
+#ifdef GR_TRACE
+static __device__ long long *g_trace;
+static __device__ int g_trace_L;
+#define GR_TSTAMP(k)                                                                         \
+    do {                                                                                    \
+        if (g_trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_L < 256) {            \
+            long long t_;                                                                   \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+            g_trace[g_trace_L * 16 + (k)] = t_;                                             \
+        }                                                                                   \
+    } while (0)
+#else
+#define GR_TSTAMP(k) do {} while (0)
+#endif
+
 // ---------------------------------------------------------------------------
 // Warp-staged append into a frontier queue (filter output).
 // All 32 lanes must call push()/finish() together (warp-converged).
 // With offsets: entries carry the exclusive prefix of their degree.
+// Entries are staged in shared memory and written kStageCap at a time, so one
+// global atomicAdd reserves up to kStageCap queue slots (the counter is a
+// single L2 address shared by the whole grid: fewer atomics, less contention).
 // ---------------------------------------------------------------------------
 struct Appender {
     int32_t *sv;                    // smem staging [kStageCap]
-    int64_t *sd;                    // smem staging degrees [kStageCap] (offsets mode)
+    int32_t *sd;                    // smem staging degrees [kStageCap] (offsets mode)
     int cnt;                        // warp-uniform
     int32_t *qv;                    // destination queue
     int64_t *qo;                    // destination prefix (null: count-only queue)
@@ -42,138 +62,243 @@ struct Appender {
     int64_t cap;                    // queue capacity
     unsigned long long *overflow;
 
-    __device__ __forceinline__ void flush(int k) {
-        unsigned l = lane_id();
-        int32_t v = 0;
-        int64_t d = 0;
-        if ((int)l < k) { v = sv[l]; if (qo) d = sd[l]; }
-        unsigned long long base = 0;
-        int64_t incl = 0, total = 0;
-        if (qo) {
-            incl = warp_incl_scan<int64_t>(d);
-            total = __shfl_sync(0xffffffffu, incl, 31);
+    __device__ __forceinline__ void flush() {
+        const unsigned l = lane_id();
+        const int k = cnt;
+        constexpr int kR = kStageCap / 32;
+        int64_t incl[kR];
+        int64_t run = 0;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            int64_t d = 0;
+            if (qo && r * 32 < k && r * 32 + (int)l < k) d = sd[r * 32 + l];
+            int64_t x = (qo && r * 32 < k) ? warp_incl_scan<int64_t>(d) : 0;
+            incl[r] = run + x - d;  // exclusive prefix of this entry
+            run += __shfl_sync(0xffffffffu, x, 31);
         }
+        unsigned long long base = 0;
         if (l == 0) {
-            unsigned long long add = qo ? (((unsigned long long)total << S) | (unsigned long long)k)
-                                        : (unsigned long long)k;
+            const unsigned long long add = qo ? (((unsigned long long)run << S) | (unsigned long long)k)
+                                              : (unsigned long long)k;
             base = atomicAdd(counter, add);
         }
         base = __shfl_sync(0xffffffffu, base, 0);
-        unsigned long long cbase = qo ? (base & ((1ull << S) - 1)) : base;
+        const unsigned long long cbase = qo ? (base & ((1ull << S) - 1)) : base;
         if ((int64_t)(cbase + k) > cap) {
             if (l == 0) atomicExch(overflow, 1ull);
-        } else if ((int)l < k) {
-            qv[cbase + l] = v;
-            if (qo) qo[cbase + l] = (int64_t)(base >> S) + (incl - d);
+        } else {
+            const int64_t ebase = (int64_t)(base >> S);
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                const int j = r * 32 + (int)l;
+                if (j < k) {
+                    qv[cbase + j] = sv[j];
+                    if (qo) qo[cbase + j] = ebase + incl[r];
+                }
+            }
         }
-    }
-
-    __device__ __forceinline__ void push(bool has, int32_t v, int64_t d) {
-        unsigned mask = __ballot_sync(0xffffffffu, has);
-        if (mask == 0) return;
-        int pos = cnt + __popc(mask & lanemask_lt());
-        if (has) { sv[pos] = v; if (qo) sd[pos] = d; }
-        cnt += __popc(mask);
-        __syncwarp();
-        if (cnt >= 32) {
-            flush(32);
-            __syncwarp();
-            unsigned l = lane_id();
-            int rest = cnt - 32;
-            int32_t tv = 0; int64_t td = 0;
-            if ((int)l < rest) { tv = sv[32 + l]; if (qo) td = sd[32 + l]; }
-            __syncwarp();
-            if ((int)l < rest) { sv[l] = tv; if (qo) sd[l] = td; }
-            __syncwarp();
-            cnt = rest;
-        }
-    }
-
-    __device__ __forceinline__ void finish() {
-        if (cnt > 0) flush(cnt);
         __syncwarp();
         cnt = 0;
     }
+
+    __device__ __forceinline__ void push(bool has, int32_t v, int64_t d) {
+        const unsigned mask = __ballot_sync(0xffffffffu, has);
+        if (mask == 0) return;
+        const int pos = cnt + __popc(mask & lanemask_lt());
+        if (has) { sv[pos] = v; if (qo) sd[pos] = (int32_t)d; }
+        cnt += __popc(mask);
+        __syncwarp();
+        if (cnt > kStageCap - 32) flush();
+    }
+
+    __device__ __forceinline__ void finish() {
+        if (cnt > 0) flush();
+        __syncwarp();
+    }
 };
 
-// Largest i in [0, F) with qo[i] <= e (qo ascending, qo[0] = 0 <= e).
+// Cache-policy loads (PTX createpolicy): the C / W streams are read once per
+// traversal and must not evict the L2-resident per-vertex state (visited
+// bitmap, depth, dist); that state is loaded with evict_last.
+__device__ __forceinline__ unsigned long long policy_evict_first() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned long long policy_evict_last() {
+    unsigned long long p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *p, unsigned long long pol) {
+    int32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+                 : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t *p, unsigned long long pol) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
+                 : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+// L2-coherent probe of state updated by other SMs during the step.
+__device__ __forceinline__ uint32_t ld_probe(const uint32_t *p, unsigned long long pol) {
+    uint32_t r;
+    asm volatile("ld.global.cg.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ unsigned long long ld_probe(const unsigned long long *p, unsigned long long pol) {
+    unsigned long long r;
+    asm volatile("ld.global.cg.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
+    return r;
+}
+
+// Smallest i in [0, F] with key(i) >= t, key non-decreasing, key(F) = +inf.
 // 32-ary cooperative search: each round narrows the range 32x.
-__device__ __forceinline__ int64_t warp_search(const int64_t *qo, int64_t F, int64_t e) {
-    int64_t lo = 0, hi = F;  // answer in [lo, hi)
-    unsigned l = lane_id();
+template <class Key>
+__device__ __forceinline__ int64_t warp_lower_bound(int64_t F, int64_t t, Key key) {
+    int64_t lo = 0, hi = F;  // answer in [lo, hi]
+    const unsigned l = lane_id();
     while (hi - lo > 32) {
-        int64_t span = hi - lo;
-        int64_t p = lo + (span * (int64_t)l) / 32;
-        int64_t val = __ldcg(qo + p);
-        unsigned b = __ballot_sync(0xffffffffu, val <= e);
-        int k = 31 - __clz(b);                      // lane 0 always qualifies
-        int64_t nlo = lo + (span * (int64_t)k) / 32;
-        int64_t nhi = (k == 31) ? hi : lo + (span * (int64_t)(k + 1)) / 32;
+        // probes p_l = lo + (l+1)*step - 1, step = floor(span/32) >= 1: shifts only
+        const int64_t step = (hi - lo) >> 5;
+        const int64_t p = lo + (int64_t)(l + 1) * step - 1;
+        const unsigned b = __ballot_sync(0xffffffffu, key(p) < t);
+        const int k = __popc(b);  // probes [0,k) are < t
+        const int64_t nlo = (k == 0) ? lo : lo + (int64_t)k * step;        // p_{k-1} + 1
+        const int64_t nhi = (k == 32) ? hi : lo + (int64_t)(k + 1) * step - 1;  // p_k
         lo = nlo; hi = nhi;
     }
-    int64_t p = lo + l;
-    bool ok = p < hi && __ldcg(qo + p) <= e;
-    unsigned b = __ballot_sync(0xffffffffu, ok);
-    return lo + (31 - __clz(b));
+    const int64_t p = lo + l;
+    const bool less = p < hi && key(p) < t;
+    return lo + __popc(__ballot_sync(0xffffffffu, less));
 }
 
 // ---------------------------------------------------------------------------
+// Frontier views: where the queue of the current level lives.
+//   GlobalFrontier: vertex ids + exclusive degree prefix in global memory,
+//                   row starts read from R (grid-wide levels).
+//   SmemFrontier:   the same three arrays in shared memory (single-CTA levels;
+//                   the row start was cached when the prefix was built).
+// ---------------------------------------------------------------------------
+struct GlobalFrontier {
+    const int32_t *qv;
+    const int64_t *qo;
+    const int64_t *R;
+    int64_t F, E;
+    __device__ __forceinline__ int64_t off(int64_t i) const { return __ldcg(qo + i); }
+    __device__ __forceinline__ void load(int64_t j, int32_t &v, int64_t &o, int64_t &rs, int64_t &end) const {
+        v = __ldcg(qv + j);
+        o = __ldcg(qo + j);
+        rs = R[v];
+        end = o + (R[v + 1] - rs);
+    }
+};
+
+struct SmemFrontier {
+    const int32_t *qv;
+    const int64_t *qo;
+    const int64_t *rs;
+    int64_t F, E;
+    __device__ __forceinline__ int64_t off(int64_t i) const { return qo[i]; }
+    __device__ __forceinline__ void load(int64_t j, int32_t &v, int64_t &o, int64_t &r, int64_t &end) const {
+        v = qv[j];
+        o = qo[j];
+        r = rs[j];
+        end = (j + 1 < F) ? qo[j + 1] : E;
+    }
+};
+
+// ---------------------------------------------------------------------------
 // Load-balanced advance over the frontier queue (merge-path).
+// The merged sequence of frontier vertices and their edges (F + E items) is
+// cut into equal pieces, one per warp (of the grid, or of one CTA), so every
+// warp gets the same number of (vertex window loads + edge visits).
 // Op must provide:
 //   uint64_t entry(int32_t v)            per-source payload (e.g. dist[v])
 //   void edges<U>(ok[], src[], pay[], dst[], eidx[])  process U edges per lane
-// Each warp of the grid processes the contiguous edge range
-//   [E*gw/nw, E*(gw+1)/nw).
 // ---------------------------------------------------------------------------
 constexpr int kUnroll = 4;
 
-template <class Op>
-__device__ __forceinline__ void expand_lb(const int32_t *__restrict__ qv, const int64_t *__restrict__ qo,
-                                          int64_t F, int64_t E, const int64_t *__restrict__ R,
-                                          const int32_t *__restrict__ C, int64_t gw, int64_t nw, Op &op) {
+template <class Front, class Op>
+__device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__restrict__ C, int64_t gw,
+                                          int64_t nw, Op &op) {
+    const int64_t F = fr.F, E = fr.E;
     if (E <= 0 || F <= 0) return;
-    int64_t e0 = (E * gw) / nw;  // E < 2^40, nw < 2^20: no overflow
-    int64_t e1 = (E * (gw + 1)) / nw;
+    const int64_t D = F + E;
+    const int64_t d0 = (D * gw) / nw;  // D < 2^40, nw < 2^20: no overflow
+    const int64_t d1 = (D * (gw + 1)) / nw;
+    if (d0 >= d1) return;
+    auto mkey = [&](int64_t i) { return fr.off(i) + i; };  // merged position of vertex i
+    const int64_t i0 = warp_lower_bound(F, d0, mkey);
+    const int64_t i1 = warp_lower_bound(F, d1, mkey);
+    GR_TSTAMP(1);
+    const int64_t e0 = d0 - i0, e1 = d1 - i1;
     if (e0 >= e1) return;
-    unsigned l = lane_id();
-    int64_t i = warp_search(qo, F, e0);
+    const unsigned l = lane_id();
+    const unsigned long long pol = policy_evict_first();
+    // owner of edge e0: largest i with qo[i] <= e0 (i0 - 1, or i0 if its list starts at e0)
+    int64_t i = (i0 < F && fr.off(i0) == e0) ? i0 : i0 - 1;
     int64_t e = e0;
     while (e < e1) {
-        int64_t j = i + l;
-        bool valid = j < F;
-        int32_t v = valid ? __ldcg(qv + j) : 0;
-        int64_t o = valid ? __ldcg(qo + j) : E;
-        int64_t rs = 0, re = 0;
-        if (valid) { rs = R[v]; re = R[v + 1]; }
-        unsigned long long pay = valid ? op.entry(v) : 0ull;
-        int64_t end = valid ? o + (re - rs) : E;
+        const int64_t j = i + l;
+        const bool valid = j < F;
+        int32_t v = 0;
+        int64_t o = E, rs = 0, end = E;
+        if (valid) fr.load(j, v, o, rs, end);
+        const unsigned long long pay = valid ? op.entry(v) : 0ull;
+        const int64_t shift = rs - o;               // C index of edge x of entry j = x + shift
         int64_t wend = __shfl_sync(0xffffffffu, end, 31);
+        GR_TSTAMP(2);
         if (wend > e1) wend = e1;
         for (int64_t b = e; b < wend; b += 32 * kUnroll) {
+            // offsets relative to the batch start fit in 32 bits (clamped)
+            const int64_t rel64 = o - b;
+            const int32_t rel = rel64 < -0x7fffffffLL ? -0x7fffffff : (rel64 > 0x7fffffffLL ? 0x7fffffff : (int32_t)rel64);
+            // uniform fast path: the whole group belongs to one entry
+            const unsigned first = __ballot_sync(0xffffffffu, rel <= 0);
+            const unsigned last = __ballot_sync(0xffffffffu, rel <= 32 * kUnroll - 1);
+            const int kf = 31 - __clz(first), kl = 31 - __clz(last);
             bool ok[kUnroll];
             int32_t src[kUnroll];
             unsigned long long sp[kUnroll];
             int64_t eidx[kUnroll];
             int32_t dst[kUnroll];
+            if (kf == kl) {
+                const int32_t sv = __shfl_sync(0xffffffffu, v, kf);
+                const unsigned long long spv = __shfl_sync(0xffffffffu, pay, kf);
+                const int64_t sh = __shfl_sync(0xffffffffu, shift, kf);
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
-                int64_t my = b + u * 32 + l;
-                int k = 0;
-#pragma unroll
-                for (int s = 16; s >= 1; s >>= 1) {
-                    int64_t oc = __shfl_sync(0xffffffffu, o, k + s);
-                    if (oc <= my) k += s;
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int64_t my = b + u * 32 + l;
+                    ok[u] = my < wend;
+                    src[u] = sv;
+                    sp[u] = spv;
+                    eidx[u] = my + sh;
                 }
-                ok[u] = my < wend;
-                src[u] = __shfl_sync(0xffffffffu, v, k);
-                sp[u] = __shfl_sync(0xffffffffu, pay, k);
-                int64_t ok_o = __shfl_sync(0xffffffffu, o, k);
-                int64_t ok_rs = __shfl_sync(0xffffffffu, rs, k);
-                eidx[u] = ok_rs + (my - ok_o);
+            } else {
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int32_t myr = u * 32 + (int32_t)l;
+                    int k = 0;
+#pragma unroll
+                    for (int s = 16; s >= 1; s >>= 1) {
+                        const int32_t oc = __shfl_sync(0xffffffffu, rel, k + s);
+                        if (oc <= myr) k += s;
+                    }
+                    const int64_t my = b + myr;
+                    ok[u] = my < wend;
+                    src[u] = __shfl_sync(0xffffffffu, v, k);
+                    sp[u] = __shfl_sync(0xffffffffu, pay, k);
+                    eidx[u] = my + __shfl_sync(0xffffffffu, shift, k);
+                }
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) dst[u] = ok[u] ? __ldg(C + eidx[u]) : 0;
+            for (int u = 0; u < kUnroll; ++u) dst[u] = ok[u] ? ld_stream(C + eidx[u], pol) : 0;
+            GR_TSTAMP(3);
             op.template edges<kUnroll>(ok, src, sp, dst, eidx);
+            GR_TSTAMP(4);
         }
         e = wend;
         i += 32;

@@ -15,9 +15,10 @@ namespace gr {
 namespace cg = cooperative_groups;
 
 constexpr int kWarp = 32;
-constexpr int kBlock = 256;              // threads per CTA of the persistent kernels
+constexpr int kBlock = 1024;             // threads per CTA of the persistent kernels
+constexpr int kMinBlocks = 1;            // resident CTAs per SM the kernels are built for
 constexpr int kWarpsPerBlock = kBlock / kWarp;
-constexpr int kStageCap = 64;            // per-warp smem staging of appended vertices
+constexpr int kStageCap = 256;           // per-warp smem staging of appended vertices
 constexpr int kMaxStatRecords = 1 << 16; // per-level records kept for gr_get_run_stats
 constexpr int kSlots = 4;                // rotating per-level control slots
 
@@ -32,6 +33,7 @@ gr_status cuda_fail(cudaError_t e, const char *what, const char *file, int line)
     } while (0)
 
 void count_launch(int k = 1);
+int64_t env_int(const char *name, int64_t dflt);  // tuning knobs
 
 // ---------------------------------------------------------------- control block
 // One slot per in-flight level (rotating, kSlots). Level L reads the frontier
@@ -53,7 +55,7 @@ struct Ctl {
     unsigned long long levels;     // levels executed by the last run
     unsigned long long reached;    // (unused by kernels; host bookkeeping)
     unsigned long long far_count[2];
-    unsigned long long pad[3];
+    long long bstate[8];           // small-mode handoff of the traversal state
 };
 
 // ---------------------------------------------------------------- graph object
@@ -76,7 +78,8 @@ struct Graph {
 
     // per-run scratch (device)
     uint32_t *visited = nullptr;  // [nwords] visited bitmap (P:793-799 culling)
-    uint32_t *fbuf[2] = {nullptr, nullptr}; // frontier bitmaps for pull
+    uint32_t *noin = nullptr;     // [nwords] vertices with in-degree 0 (never discoverable)
+    uint32_t *fbuf[3] = {nullptr, nullptr, nullptr}; // rotating frontier bitmaps
     int32_t *qv[2] = {nullptr, nullptr};    // frontier queues (vertex ids)
     int64_t *qo[2] = {nullptr, nullptr};    // exclusive prefix of degrees
     int32_t *depth_buf = nullptr; // internal outputs when caller passes host memory
@@ -117,6 +120,11 @@ __device__ __forceinline__ unsigned lanemask_lt() {
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned long long ld_cg(const unsigned long long *p) {
     return __ldcg(p);
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+    unsigned long long r;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+    return r;
 }
 __device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long *p) {
     return *(volatile const unsigned long long *)p;

@@ -23,7 +23,7 @@ gr_status dev_alloc(Graph *g, void **p, size_t bytes) {
 
 void dev_free_all(Graph *g) {
     void *ptrs[] = {g->R, g->C, g->W, (g->Rt != g->R) ? g->Rt : nullptr,
-                    (g->Ct != g->C) ? g->Ct : nullptr, g->visited, g->fbuf[0], g->fbuf[1],
+                    (g->Ct != g->C) ? g->Ct : nullptr, g->visited, g->noin, g->fbuf[0], g->fbuf[1], g->fbuf[2],
                     g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->depth_buf, g->pred_buf,
                     g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev};
     for (void *p : ptrs)
@@ -94,6 +94,21 @@ __global__ void csc_scatter_kernel(const int64_t *R, const int32_t *C, int64_t n
             unsigned long long p = atomicAdd(cursor + C[e], 1ull);
             Ct[p] = (int32_t)u;
         }
+}
+
+// bitmap of vertices with no in-edge (never discoverable by a traversal)
+__global__ void noin_kernel(const int64_t *Rt, int64_t n, uint32_t *noin) {
+    int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    int64_t nw = (n + 31) / 32;
+    for (int64_t w = tid; w < nw; w += nt) {
+        uint32_t bits = 0;
+        for (int b = 0; b < 32; ++b) {
+            int64_t v = w * 32 + b;
+            if (v < n && Rt[v + 1] == Rt[v]) bits |= 1u << b;
+        }
+        noin[w] = bits;
+    }
 }
 
 static bool is_device_ptr(const void *p) {
@@ -214,8 +229,11 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
     // per-run scratch for BFS (SSSP scratch is allocated on first use)
     const int64_t nw = (n + 31) / 32;
     TRY(dev_alloc(g, (void **)&g->visited, nw * sizeof(uint32_t)));
-    TRY(dev_alloc(g, (void **)&g->fbuf[0], nw * sizeof(uint32_t)));
-    TRY(dev_alloc(g, (void **)&g->fbuf[1], nw * sizeof(uint32_t)));
+    TRY(dev_alloc(g, (void **)&g->noin, nw * sizeof(uint32_t)));
+    noin_kernel<<<blocks, 256, 0, s>>>(g->Rt, n, g->noin);
+    count_launch();
+    TRYC(cudaGetLastError());
+    for (int i = 0; i < 3; ++i) TRY(dev_alloc(g, (void **)&g->fbuf[i], nw * sizeof(uint32_t)));
     for (int i = 0; i < 2; ++i) {
         TRY(dev_alloc(g, (void **)&g->qv[i], n * sizeof(int32_t)));
         TRY(dev_alloc(g, (void **)&g->qo[i], n * sizeof(int64_t)));

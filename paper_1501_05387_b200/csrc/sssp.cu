@@ -21,15 +21,23 @@ struct SsspArgs {
     const uint32_t *W;
     unsigned long long *dp;   // (dist << 32) | pred
     int32_t *stamp;
-    int32_t *qv0, *qv1;
-    int64_t *qo0, *qo1;
-    int32_t *far0, *far1;
+    int32_t *qv[2];
+    int64_t *qo[2];
+    int32_t *far[2];
     int64_t far_cap;
     Ctl *ctl;
     gr_level_stats *stats;
     int32_t src;
     uint64_t delta;
     int S;
+};
+
+struct SsspSmem {
+    int32_t sv[kWarpsPerBlock][kStageCap];   // near staging
+    int32_t sd[kWarpsPerBlock][kStageCap];
+    int32_t fv[kWarpsPerBlock][kStageCap];   // far staging
+    unsigned long long ctl[8];
+    unsigned long long bsum[4];
 };
 
 // Fused advance + compute + filter of one near iteration (a10).
@@ -43,9 +51,11 @@ struct RelaxOp {
     Appender *nearq;
     Appender *farq;
     unsigned long long nimp;
+    unsigned long long pol_w;     // evict_first for the weight stream
+    unsigned long long pol_keep;  // evict_last for dist
 
     __device__ __forceinline__ unsigned long long entry(int32_t v) {
-        return ld_cg(dp + v) >> 32;  // dist[u] read when the window is loaded
+        return ld_probe(dp + v, pol_keep) >> 32;  // dist[u] read when the window is loaded
     }
 
     template <int U>
@@ -55,8 +65,8 @@ struct RelaxOp {
         unsigned long long cur[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            w[u] = ok[u] ? __ldg(W + eidx[u]) : 0u;
-            cur[u] = ok[u] ? ld_cg(dp + dst[u]) : 0ull;
+            w[u] = ok[u] ? ld_stream(W + eidx[u], pol_w) : 0u;
+            cur[u] = ok[u] ? ld_probe(dp + dst[u], pol_keep) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -83,11 +93,16 @@ struct RelaxOp {
     }
 };
 
-__global__ void __launch_bounds__(kBlock) sssp_kernel(SsspArgs a) {
+__device__ __forceinline__ long long sssp_gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
     cg::grid_group grid = cg::this_grid();
-    __shared__ int32_t s_v[kWarpsPerBlock][kStageCap];
-    __shared__ int64_t s_d[kWarpsPerBlock][kStageCap];
-    __shared__ int32_t s_fv[kWarpsPerBlock][kStageCap];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SsspSmem *s = reinterpret_cast<SsspSmem *>(smem_raw);
 
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -113,33 +128,50 @@ __global__ void __launch_bounds__(kBlock) sssp_kernel(SsspArgs a) {
         const int64_t d = a.R[a.src + 1] - a.R[a.src];
         a.dp[a.src] = (unsigned long long)(unsigned int)a.src;  // dist 0, pred = src (A-1)
         if (d > 0) {
-            a.qv0[0] = a.src;
-            a.qo0[0] = 0;
+            a.qv[0][0] = a.src;
+            a.qo[0][0] = 0;
             a.ctl->slot[0].qpack = ((unsigned long long)d << a.S) | 1ull;
         }
     }
     grid.sync();
 
     Appender nearq, farq;
-    nearq.sv = s_v[wib]; nearq.sd = s_d[wib]; nearq.cnt = 0; nearq.S = a.S; nearq.cap = a.n;
+    nearq.sv = s->sv[wib]; nearq.sd = s->sd[wib]; nearq.cnt = 0; nearq.S = a.S; nearq.cap = a.n;
     nearq.overflow = &a.ctl->overflow;
-    farq.sv = s_fv[wib]; farq.sd = nullptr; farq.cnt = 0; farq.qo = nullptr; farq.S = 0;
+    farq.sv = s->fv[wib]; farq.sd = nullptr; farq.cnt = 0; farq.qo = nullptr; farq.S = 0;
     farq.cap = a.far_cap; farq.overflow = &a.ctl->overflow;
+    const unsigned long long pol_w = policy_evict_first();
+    const unsigned long long pol_keep = policy_evict_last();
 
     uint64_t thr = a.delta;          // near band is [.., thr)
     int32_t it = 0;                  // stamp iteration (keys 2*it, 2*it+1)
     int fp = 0;                      // current far buffer
     int k = 0;                       // step index (slots, queue ping-pong)
+    long long t_prev = 0;
+    if (tid == 0) t_prev = sssp_gtimer();
     for (;; ++k) {
         Slot &cur = a.ctl->slot[k & 3];
         Slot &nxt = a.ctl->slot[(k + 1) & 3];
-        const unsigned long long qp = ld_volatile(&cur.qpack);
+        // ---- control words: one thread reads, the CTA shares ----------------
+        if (threadIdx.x == 0) {
+            s->ctl[0] = ld_volatile(&cur.qpack);
+            s->ctl[1] = ld_volatile(&a.ctl->far_count[fp]);
+            s->ctl[2] = ld_volatile(&cur.ndisc);
+            s->ctl[3] = ld_volatile(&a.ctl->overflow);
+            s->bsum[0] = 0;
+        }
+        __syncthreads();
+        const unsigned long long qp = s->ctl[0];
         const int64_t f = (int64_t)(qp & cmask);
         const int64_t mf = (int64_t)(qp >> a.S);
-        const int64_t fc = (int64_t)ld_volatile(&a.ctl->far_count[fp]);
-        if (k > 0 && tid == 0 && k - 1 < kMaxStatRecords)
-            a.stats[k - 1].discovered = (int64_t)ld_volatile(&cur.ndisc);
-        if (ld_volatile(&a.ctl->overflow)) break;
+        const int64_t fc = (int64_t)s->ctl[1];
+        if (k > 0 && tid == 0 && k - 1 < kMaxStatRecords) {
+            a.stats[k - 1].discovered = (int64_t)s->ctl[2];
+            const long long t = sssp_gtimer();
+            a.stats[k - 1].ns = t - t_prev;
+            t_prev = t;
+        }
+        if (s->ctl[3]) break;
         if (f == 0 && fc == 0) break;
         if (tid == 0) {
             Slot &rst = a.ctl->slot[(k + 2) & 3];
@@ -149,48 +181,62 @@ __global__ void __launch_bounds__(kBlock) sssp_kernel(SsspArgs a) {
                 gr_level_stats &st = a.stats[k];
                 st.level = k; st.direction = f > 0 ? 3 : 4; st.frontier = f > 0 ? f : fc;
                 st.frontier_edges = mf; st.discovered = 0; st.inspected_edges = mf; st.aux = fc;
+                st.ns = 0;
             }
         }
-        int32_t *qv_c = (k & 1) ? a.qv1 : a.qv0;
-        int64_t *qo_c = (k & 1) ? a.qo1 : a.qo0;
-        nearq.qv = (k & 1) ? a.qv0 : a.qv1;
-        nearq.qo = (k & 1) ? a.qo0 : a.qo1;
+        nearq.qv = a.qv[(k + 1) & 1];
+        nearq.qo = a.qo[(k + 1) & 1];
         nearq.counter = &nxt.qpack;
 
         if (f > 0) {
             // ---- near iteration: Advance(UpdateLabel, SetPred) + Filter ----
             ++it;
-            farq.qv = fp ? a.far1 : a.far0;
+            farq.qv = a.far[fp];
             farq.counter = &a.ctl->far_count[fp];
-            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull};
-            expand_lb(qv_c, qo_c, f, mf, a.R, a.C, gw, nw, op);
+            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_w, pol_keep};
+            GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.R, f, mf};
+            expand_lb(fr, a.C, gw, nw, op);
             nearq.finish();
             farq.finish();
-            unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
-            if (lane_id() == 0 && ni) atomicAdd(&nxt.ndisc, ni);
+            const unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
+            if (lane_id() == 0 && ni) atomicAdd(&s->bsum[0], ni);
+            __syncthreads();
+            if (threadIdx.x == 0 && s->bsum[0]) atomicAdd(&nxt.ndisc, s->bsum[0]);
             grid.sync();
         } else {
             // ---- near slice exhausted: "update the priority function and
             // operate on the far slice". Re-split (A-11). --------
-            const int32_t *far_c = fp ? a.far1 : a.far0;
+            const int32_t *far_c = a.far[fp];
+            if (threadIdx.x == 0) s->bsum[1] = ~0ull;
+            __syncthreads();
+            unsigned long long mymin = ~0ull;
             for (int64_t j = tid; j < fc; j += nthreads) {
                 const int32_t v = far_c[j];
-                const unsigned long long d = ld_cg(a.dp + v) >> 32;
-                if (d >= thr) atomicMin(&cur.minfar, d);
+                const unsigned long long d = ld_probe(a.dp + v, pol_keep) >> 32;
+                if (d >= thr && d < mymin) mymin = d;
             }
+            for (int sh = 16; sh > 0; sh >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, mymin, sh);
+                mymin = o < mymin ? o : mymin;
+            }
+            if (lane_id() == 0 && mymin != ~0ull) atomicMin(&s->bsum[1], mymin);
+            __syncthreads();
+            if (threadIdx.x == 0 && s->bsum[1] != ~0ull) atomicMin(&cur.minfar, s->bsum[1]);
             grid.sync();
-            const unsigned long long mn = ld_volatile(&cur.minfar);
+            if (threadIdx.x == 0) s->ctl[4] = ld_volatile(&cur.minfar);
             if (tid == 0) a.ctl->far_count[fp] = 0ull;
+            __syncthreads();
+            const unsigned long long mn = s->ctl[4];
             if (mn == ~0ull) {  // every far entry was stale: the next step
                 grid.sync();        // sees f == 0 and an empty far pile and stops
                 fp ^= 1;
                 continue;
             }
             const uint64_t thr_old = thr;
-            uint64_t band = (mn / a.delta + 1);
+            const uint64_t band = (mn / a.delta + 1);
             thr = (band > (0xFFFFFFFFFFFFFFFFull / a.delta)) ? 0xFFFFFFFFFFFFFFFFull : band * a.delta;
             ++it;
-            farq.qv = fp ? a.far0 : a.far1;
+            farq.qv = a.far[fp ^ 1];
             farq.counter = &a.ctl->far_count[fp ^ 1];
             for (int64_t base = gw * 32; base < fc; base += nw * 32) {
                 const int64_t j = base + lane_id();
@@ -199,7 +245,7 @@ __global__ void __launch_bounds__(kBlock) sssp_kernel(SsspArgs a) {
                 int64_t deg = 0;
                 if (j < fc) {
                     v = far_c[j];
-                    const unsigned long long d = ld_cg(a.dp + v) >> 32;
+                    const unsigned long long d = ld_probe(a.dp + v, pol_keep) >> 32;
                     if (d >= thr_old) {  // else stale: already expanded below thr_old
                         const bool nearb = d < thr;
                         const int32_t key = 2 * it + (nearb ? 0 : 1);
@@ -236,20 +282,22 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.n = g->n; a.m = g->m;
     a.R = g->R; a.C = g->C; a.W = g->W;
     a.dp = g->dp; a.stamp = g->stamp;
-    a.qv0 = g->qv[0]; a.qv1 = g->qv[1];
-    a.qo0 = g->qo[0]; a.qo1 = g->qo[1];
-    a.far0 = g->farq[0]; a.far1 = g->farq[1];
+    for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.far[i] = g->farq[i]; }
     a.far_cap = g->far_cap;
     a.ctl = g->ctl; a.stats = g->stats_dev;
     a.src = src;
     a.delta = delta;
     a.S = g->pack_shift;
-    int per_sm = 0;
-    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sssp_kernel, kBlock, 0));
+    static int per_sm = 0;
+    const size_t smem = sizeof(SsspSmem);
+    if (per_sm == 0) {
+        GR_CUDA(cudaFuncSetAttribute(sssp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sssp_kernel, kBlock, smem));
+    }
     if (per_sm < 1) { set_error("sssp_kernel cannot be resident"); return GR_ERR_CUDA; }
     dim3 grid(g->num_sms * per_sm), block(kBlock);
     void *args[] = {&a};
-    GR_CUDA(cudaLaunchCooperativeKernel((void *)sssp_kernel, grid, block, args, 0, g->stream));
+    GR_CUDA(cudaLaunchCooperativeKernel((void *)sssp_kernel, grid, block, args, smem, g->stream));
     unpack_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->dp, g->n, dist, pred);
     GR_CUDA(cudaGetLastError());
     count_launch(2);
