@@ -16,7 +16,7 @@ import os
 from typing import Optional
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgr_b200.so")
+LIB_PATH = os.path.join(_HERE, os.environ.get("GR_LIB", "libgr_b200.so"))  # GR_LIB: tuning builds
 
 GR_OK = 0
 GR_SYMMETRIC = 1

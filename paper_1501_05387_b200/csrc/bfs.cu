@@ -24,9 +24,16 @@
 
 namespace gr {
 
-constexpr int64_t kSmallF = 4096;   // small mode: queue capacity (shared memory)
+#ifndef GR_SMALL_CAP
+#define GR_SMALL_CAP 2048
+#endif
+constexpr int64_t kSmallF = GR_SMALL_CAP;  // small mode: queue capacity (shared memory)
 constexpr int64_t kSmallFDefault = 1024;  // small mode: default max frontier (swept on C4)
 constexpr int64_t kSmallE = 16384;  // small mode: max frontier edges
+#ifndef GR_BFS_STAGES
+#define GR_BFS_STAGES 0  // measured on C2 push: 2 and 4 stages are slower (smem displaces L1)
+#endif
+constexpr int kBfsStages = GR_BFS_STAGES;  // cp.async pipeline depth of the grid push advance (0: off)
 constexpr int kSmallCntBits = 24;   // count field of the small-mode packed counter
 constexpr unsigned long long kSmallCntMask = (1ull << kSmallCntBits) - 1;
 
@@ -57,7 +64,8 @@ struct BfsArgs {
 
 struct BfsSmem {
     union {
-        struct {  // grid levels: per-warp append staging
+        struct {  // grid levels: per-warp append staging + cp.async pipeline
+            PipeWarpSmem<(kBfsStages > 0 ? kBfsStages : 1), false> pipe[kBfsStages > 0 ? kWarpsPerBlock : 1];
             int32_t sv[kWarpsPerBlock][kStageCap];
             int32_t sd[kWarpsPerBlock][kStageCap];
         } stage;
@@ -98,19 +106,22 @@ struct BfsPushOp {
     Appender *app;
     unsigned long long ndisc;
     unsigned long long pol_keep;   // evict_last policy for the visited bitmap
-    bool probe;          // culling probe before the claim (big levels); small levels
-                         // claim directly: one L2 round trip less on the critical path
+    int probe;           // culling probe before the claim: 0 none (small levels claim
+                         // directly: one L2 round trip less on the critical path),
+                         // 1 L2-coherent, 2 through L1 (most targets already visited
+                         // before the level: L1 hits, stale words only cost an atomic)
 
     __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
 
-    template <int U>
+    template <int U, class T5>
     __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *,
-                                          const int32_t *dst, const int64_t *) {
+                                          const int32_t *dst, const T5 *) {
         uint32_t word[U];
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            word[u] = (ok[u] && probe) ? ld_probe(visited + (dst[u] >> 5), pol_keep)
-                                       : (ok[u] ? 0u : 0xffffffffu);
+            word[u] = !ok[u] ? 0xffffffffu
+                    : probe == 1 ? ld_probe(visited + (dst[u] >> 5), pol_keep)
+                    : probe == 2 ? ld_l1(visited + (dst[u] >> 5)) : 0u;
         bool disc[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -594,9 +605,14 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
             for (int64_t w = tid; w < nwords; w += nthreads) fb_z[w] = 0u;
         if (dir == 1) {
             BfsPushOp op{a.visited, st.fbn_clean ? fb_n : nullptr, a.depth, a.pred, a.R, L + 1,
-                         a.idempotent, &app, 0ull, pol_keep, mf >= (1 << 16)};
+                         a.idempotent, &app, 0ull, pol_keep,
+                         mf < (1 << 16) ? 0 : (st.m_u * 4 < a.m ? 2 : 1)};
             GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.R, f, mf};
+#if GR_BFS_STAGES > 0
+            expand_pipe<kBfsStages, false>(fr, a.C, nullptr, gw, nw, op, &s->u.stage.pipe[wib]);
+#else
             expand_lb(fr, a.C, gw, nw, op);
+#endif
             ndisc = op.ndisc;
             st.fb_valid = st.fbn_clean;
         } else {

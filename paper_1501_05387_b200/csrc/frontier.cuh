@@ -51,9 +51,10 @@ static __device__ int g_trace_L;
 // global atomicAdd reserves up to kStageCap queue slots (the counter is a
 // single L2 address shared by the whole grid: fewer atomics, less contention).
 // ---------------------------------------------------------------------------
-struct Appender {
-    int32_t *sv;                    // smem staging [kStageCap]
-    int32_t *sd;                    // smem staging degrees [kStageCap] (offsets mode)
+template <int kCap>
+struct AppenderT {
+    int32_t *sv;                    // smem staging [kCap]
+    int32_t *sd;                    // smem staging degrees [kCap] (offsets mode)
     int cnt;                        // warp-uniform
     int32_t *qv;                    // destination queue
     int64_t *qo;                    // destination prefix (null: count-only queue)
@@ -65,7 +66,7 @@ struct Appender {
     __device__ __forceinline__ void flush() {
         const unsigned l = lane_id();
         const int k = cnt;
-        constexpr int kR = kStageCap / 32;
+        constexpr int kR = kCap / 32;
         int64_t incl[kR];
         int64_t run = 0;
 #pragma unroll
@@ -108,7 +109,7 @@ struct Appender {
         if (has) { sv[pos] = v; if (qo) sd[pos] = (int32_t)d; }
         cnt += __popc(mask);
         __syncwarp();
-        if (cnt > kStageCap - 32) flush();
+        if (cnt > kCap - 32) flush();
     }
 
     __device__ __forceinline__ void finish() {
@@ -116,6 +117,7 @@ struct Appender {
         __syncwarp();
     }
 };
+using Appender = AppenderT<kStageCap>;
 
 // Cache-policy loads (PTX createpolicy): the C / W streams are read once per
 // traversal and must not evict the L2-resident per-vertex state (visited
@@ -140,6 +142,13 @@ __device__ __forceinline__ uint32_t ld_stream(const uint32_t *p, unsigned long l
     uint32_t r;
     asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;"
                  : "=r"(r) : "l"(p), "l"(pol));
+    return r;
+}
+// L1-allocating probe: may return a stale (older) word; used only as a filter
+// where the bits it can miss are re-checked by an atomic.
+__device__ __forceinline__ uint32_t ld_l1(const uint32_t *p) {
+    uint32_t r;
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(r) : "l"(p));
     return r;
 }
 // L2-coherent probe of state updated by other SMs during the step.
@@ -249,6 +258,10 @@ __device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__rest
         if (valid) fr.load(j, v, o, rs, end);
         const unsigned long long pay = valid ? op.entry(v) : 0ull;
         const int64_t shift = rs - o;               // C index of edge x of entry j = x + shift
+        if (valid && end > o) {                     // first lines of every list of the window
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs));
+            if (end - o > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs + 32));
+        }
         int64_t wend = __shfl_sync(0xffffffffu, end, 31);
         GR_TSTAMP(2);
         if (wend > e1) wend = e1;
@@ -269,6 +282,9 @@ __device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__rest
                 const int32_t sv = __shfl_sync(0xffffffffu, v, kf);
                 const unsigned long long spv = __shfl_sync(0xffffffffu, pay, kf);
                 const int64_t sh = __shfl_sync(0xffffffffu, shift, kf);
+                // stream ahead: the group after next (4 lines) into L2
+                const int64_t pf = b + 2 * 32 * kUnroll + (int64_t)l * 32;
+                if (l < kUnroll && pf < wend) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + pf + sh));
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
                     const int64_t my = b + u * 32 + l;
@@ -302,6 +318,190 @@ __device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__rest
         }
         e = wend;
         i += 32;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pipelined load-balanced advance (grid levels). Same merge-path partition
+// and owner mapping as expand_lb, but the neighbour ids (and weights) of the
+// next kStages groups of 128 edges are copied global -> shared memory with
+// cp.async (LDGSTS) while the current group is processed: the per-SM bytes in
+// flight no longer depend on registers (64 per thread at 32 warps/SM), which
+// made the C stream latency-bound. A group owned by one list (hub vertices:
+// most edges of a power-law graph) is copied as 16-byte chunks of the aligned
+// superset of its range; a mixed group element by element.
+// ---------------------------------------------------------------------------
+constexpr int kGroup = 32 * kUnroll;          // edges per group
+constexpr int kGroupBuf = kGroup + 8;         // aligned superset (16-byte chunks)
+
+struct PipeStageMeta {
+    long long b;       // first edge (frontier-edge index) of the group
+    long long lim;     // end of the valid range of the group
+    int mode;          // >= 0: single owner, element k at buf[mode + k]; -1: mixed
+    int src;           // single owner vertex
+    unsigned pay;      // single owner payload
+    int pad;
+};
+
+template <int kStages, bool kW>   // kW: weights + per-source payload (SSSP)
+struct PipeWarpSmem {
+    int32_t dst[kStages][kGroupBuf];
+    int32_t wt[kW ? kStages : 1][kW ? kGroupBuf : 4];
+    int32_t src[kStages][kGroup];
+    uint32_t pay[kW ? kStages : 1][kW ? kGroup : 4];
+    PipeStageMeta meta[kStages];
+};
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global.L2::128B [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+    switch (n) {
+        case 0: cp_async_wait<0>(); break;
+        case 1: cp_async_wait<1>(); break;
+        case 2: cp_async_wait<2>(); break;
+        case 3: cp_async_wait<3>(); break;
+        case 4: cp_async_wait<4>(); break;
+        case 5: cp_async_wait<5>(); break;
+        case 6: cp_async_wait<6>(); break;
+        default: cp_async_wait<7>(); break;
+    }
+}
+
+// Op must provide entry(v) (payload, low 32 bits used) and
+//   edges<U>(ok[], src[], pay[], dst[], wt[])
+template <int kStages, bool kW, class Front, class Op>
+__device__ __forceinline__ void expand_pipe(const Front &fr, const int32_t *__restrict__ C,
+                                            const uint32_t *__restrict__ W, int64_t gw, int64_t nw,
+                                            Op &op, PipeWarpSmem<kStages, kW> *ps) {
+    const int64_t F = fr.F, E = fr.E;
+    if (E <= 0 || F <= 0) return;
+    const int64_t D = F + E;
+    const int64_t d0 = (D * gw) / nw;
+    const int64_t d1 = (D * (gw + 1)) / nw;
+    if (d0 >= d1) return;
+    auto mkey = [&](int64_t i) { return fr.off(i) + i; };
+    const int64_t i0 = warp_lower_bound(F, d0, mkey);
+    const int64_t i1 = warp_lower_bound(F, d1, mkey);
+    const int64_t e0 = d0 - i0, e1 = d1 - i1;
+    if (e0 >= e1) return;
+    const unsigned l = lane_id();
+
+    // ---- generator state: current window of 32 frontier entries -------------
+    int64_t gi = (i0 < F && fr.off(i0) == e0) ? i0 : i0 - 1;
+    int32_t v = 0;
+    int64_t o = E, shift = 0, wend = E;
+    uint32_t pay = 0;
+    auto load_window = [&]() {
+        const int64_t j = gi + l;
+        const bool valid = j < F;
+        int64_t rs = 0, end = E;
+        v = 0;
+        o = E;
+        if (valid) fr.load(j, v, o, rs, end);
+        pay = valid ? (uint32_t)op.entry(v) : 0u;
+        shift = rs - o;
+        wend = __shfl_sync(0xffffffffu, end, 31);
+        if (wend > e1) wend = e1;
+    };
+    load_window();
+    int64_t b = e0;  // next edge to issue
+
+    auto issue = [&](int s) -> bool {
+        while (b >= wend) {
+            if (b >= e1) return false;
+            gi += 32;
+            load_window();
+        }
+        const int64_t lim = (wend < b + kGroup) ? wend : b + kGroup;
+        const int64_t rel64 = o - b;
+        const int32_t rel = rel64 < -0x7fffffffLL ? -0x7fffffff
+                          : (rel64 > 0x7fffffffLL ? 0x7fffffff : (int32_t)rel64);
+        const unsigned first = __ballot_sync(0xffffffffu, rel <= 0);
+        const unsigned last = __ballot_sync(0xffffffffu, rel <= (int32_t)(lim - b) - 1);
+        const int kf = 31 - __clz(first), kl = 31 - __clz(last);
+        PipeStageMeta m;
+        m.b = b;
+        m.lim = lim;
+        if (kf == kl) {
+            const int64_t sh = __shfl_sync(0xffffffffu, shift, kf);
+            m.src = __shfl_sync(0xffffffffu, v, kf);
+            m.pay = __shfl_sync(0xffffffffu, pay, kf);
+            const int64_t g0 = b + sh;           // C index of the first edge
+            const int64_t A = g0 & ~3ll;         // 16-byte aligned start
+            m.mode = (int)(g0 - A);
+            const int n16 = (int)((m.mode + (lim - b) + 3) >> 2);  // <= 33 chunks
+            for (int c = (int)l; c < n16; c += 32) {
+                cp_async16(&ps->dst[s][4 * c], C + A + 4 * c);
+                if (kW) cp_async16(&ps->wt[kW ? s : 0][4 * c], W + A + 4 * c);
+            }
+        } else {
+            m.mode = -1;
+            m.src = 0;
+            m.pay = 0;
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int32_t myr = u * 32 + (int32_t)l;
+                int k = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const int32_t oc = __shfl_sync(0xffffffffu, rel, k + st);
+                    if (oc <= myr) k += st;
+                }
+                const int64_t my = b + myr;
+                const int32_t sv = __shfl_sync(0xffffffffu, v, k);
+                const uint32_t spv = __shfl_sync(0xffffffffu, pay, k);
+                const int64_t ci = my + __shfl_sync(0xffffffffu, shift, k);
+                if (my < lim) {
+                    cp_async4(&ps->dst[s][myr], C + ci);
+                    if (kW) cp_async4(&ps->wt[kW ? s : 0][myr], W + ci);
+                    ps->src[s][myr] = sv;
+                    if (kW) ps->pay[kW ? s : 0][myr] = spv;
+                }
+            }
+        }
+        cp_async_commit();
+        if (l == 0) ps->meta[s] = m;
+        b = lim;
+        return true;
+    };
+
+    int issued = 0, consumed = 0;
+    for (int s = 0; s < kStages; ++s) {
+        if (!issue(s)) break;
+        ++issued;
+    }
+    while (consumed < issued) {
+        const int s = consumed % kStages;
+        cp_async_wait_dyn(issued - consumed - 1);
+        __syncwarp();
+        const PipeStageMeta m = ps->meta[s];
+        bool ok[kUnroll];
+        int32_t src[kUnroll], dst[kUnroll];
+        unsigned long long pp[kUnroll];
+        uint32_t wt[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int k = u * 32 + (int)l;
+            ok[u] = m.b + k < m.lim;
+            const int idx = m.mode >= 0 ? m.mode + k : k;
+            dst[u] = ok[u] ? ps->dst[s][idx] : 0;
+            wt[u] = (kW && ok[u]) ? (uint32_t)ps->wt[kW ? s : 0][idx] : 0u;
+            src[u] = m.mode >= 0 ? m.src : (ok[u] ? ps->src[s][k] : 0);
+            pp[u] = !kW ? 0ull : (m.mode >= 0 ? m.pay : (ok[u] ? ps->pay[kW ? s : 0][k] : 0u));
+        }
+        __syncwarp();  // stage s may be refilled below
+        ++consumed;
+        if (issue(issued % kStages)) ++issued;
+        op.template edges<kUnroll>(ok, src, pp, dst, wt);
     }
 }
 

@@ -15,10 +15,19 @@ namespace gr {
 namespace cg = cooperative_groups;
 
 constexpr int kWarp = 32;
-constexpr int kBlock = 1024;             // threads per CTA of the persistent kernels
-constexpr int kMinBlocks = 1;            // resident CTAs per SM the kernels are built for
+#ifndef GR_BLOCK
+#define GR_BLOCK 512   // 512 x 2 CTAs/SM measured best of {1024x1, 512x2, 256x4} (C2, C4)
+#endif
+constexpr int kBlock = GR_BLOCK;         // threads per CTA of the persistent kernels
+#ifndef GR_MINB
+#define GR_MINB 2
+#endif
+constexpr int kMinBlocks = GR_MINB;      // resident CTAs per SM the kernels are built for
 constexpr int kWarpsPerBlock = kBlock / kWarp;
-constexpr int kStageCap = 256;           // per-warp smem staging of appended vertices
+#ifndef GR_STAGE_CAP
+#define GR_STAGE_CAP 256
+#endif
+constexpr int kStageCap = GR_STAGE_CAP;  // per-warp smem staging of appended vertices
 constexpr int kMaxStatRecords = 1 << 16; // per-level records kept for gr_get_run_stats
 constexpr int kSlots = 4;                // rotating per-level control slots
 

@@ -146,11 +146,13 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
 #define TRYC(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { st = cuda_fail(e_, #x, __FILE__, __LINE__); dev_free_all(g); delete g; return st; } } while (0)
     cudaStream_t s = g->stream;
     TRY(dev_alloc(g, (void **)&g->R, (n + 1) * sizeof(int64_t)));
-    TRY(dev_alloc(g, (void **)&g->C, m * sizeof(int32_t)));
+    // +16 B: the 16-byte cp.async chunks of the advance may read up to 12 B past
+    // the last list (values unused)
+    TRY(dev_alloc(g, (void **)&g->C, m * sizeof(int32_t) + 16));
     TRYC(cudaMemcpyAsync(g->R, R, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, s));
     if (m) TRYC(cudaMemcpyAsync(g->C, C, m * sizeof(int32_t), cudaMemcpyDefault, s));
     if (W) {
-        TRY(dev_alloc(g, (void **)&g->W, m * sizeof(uint32_t)));
+        TRY(dev_alloc(g, (void **)&g->W, m * sizeof(uint32_t) + 16));
         if (m) TRYC(cudaMemcpyAsync(g->W, W, m * sizeof(uint32_t), cudaMemcpyDefault, s));
     }
     unsigned long long *tmp = nullptr;  // 4 scratch words

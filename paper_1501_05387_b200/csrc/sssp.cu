@@ -32,10 +32,15 @@ struct SsspArgs {
     int S;
 };
 
+constexpr int kSsspStages = 2;     // cp.async pipeline depth (C + W + payload per stage)
+constexpr int kSsspStage = 128;    // append staging per warp (near and far)
+using SsspAppender = AppenderT<kSsspStage>;
+
 struct SsspSmem {
-    int32_t sv[kWarpsPerBlock][kStageCap];   // near staging
-    int32_t sd[kWarpsPerBlock][kStageCap];
-    int32_t fv[kWarpsPerBlock][kStageCap];   // far staging
+    PipeWarpSmem<kSsspStages, true> pipe[kWarpsPerBlock];
+    int32_t sv[kWarpsPerBlock][kSsspStage];   // near staging
+    int32_t sd[kWarpsPerBlock][kSsspStage];
+    int32_t fv[kWarpsPerBlock][kSsspStage];   // far staging
     unsigned long long ctl[8];
     unsigned long long bsum[4];
 };
@@ -48,26 +53,22 @@ struct RelaxOp {
     const int64_t *R;
     uint64_t thr;
     int32_t key_near;   // 2*it   (A-7)
-    Appender *nearq;
-    Appender *farq;
+    SsspAppender *nearq;
+    SsspAppender *farq;
     unsigned long long nimp;
-    unsigned long long pol_w;     // evict_first for the weight stream
     unsigned long long pol_keep;  // evict_last for dist
 
     __device__ __forceinline__ unsigned long long entry(int32_t v) {
         return ld_probe(dp + v, pol_keep) >> 32;  // dist[u] read when the window is loaded
     }
 
+    // w[]: the edge weights, staged in shared memory by the pipelined advance
     template <int U>
     __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *du,
-                                          const int32_t *dst, const int64_t *eidx) {
-        uint32_t w[U];
+                                          const int32_t *dst, const uint32_t *w) {
         unsigned long long cur[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            w[u] = ok[u] ? ld_stream(W + eidx[u], pol_w) : 0u;
-            cur[u] = ok[u] ? ld_probe(dp + dst[u], pol_keep) : 0ull;
-        }
+        for (int u = 0; u < U; ++u) cur[u] = ok[u] ? ld_probe(dp + dst[u], pol_keep) : 0ull;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             bool to_near = false, to_far = false;
@@ -135,12 +136,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
     }
     grid.sync();
 
-    Appender nearq, farq;
+    SsspAppender nearq, farq;
     nearq.sv = s->sv[wib]; nearq.sd = s->sd[wib]; nearq.cnt = 0; nearq.S = a.S; nearq.cap = a.n;
     nearq.overflow = &a.ctl->overflow;
     farq.sv = s->fv[wib]; farq.sd = nullptr; farq.cnt = 0; farq.qo = nullptr; farq.S = 0;
     farq.cap = a.far_cap; farq.overflow = &a.ctl->overflow;
-    const unsigned long long pol_w = policy_evict_first();
     const unsigned long long pol_keep = policy_evict_last();
 
     uint64_t thr = a.delta;          // near band is [.., thr)
@@ -193,9 +193,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             ++it;
             farq.qv = a.far[fp];
             farq.counter = &a.ctl->far_count[fp];
-            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_w, pol_keep};
+            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.R, f, mf};
-            expand_lb(fr, a.C, gw, nw, op);
+            expand_pipe<kSsspStages, true>(fr, a.C, a.W, gw, nw, op, &s->pipe[wib]);
             nearq.finish();
             farq.finish();
             const unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
