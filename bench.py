@@ -59,7 +59,13 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
-    return ap.parse_args()
+    ap.add_argument("--partitioned", action="store_true",
+                    help="1D-partitioned BFS over all ranks (NCCL exchange per level); "
+                         "default graph c5_kron25")
+    a = ap.parse_args()
+    if a.partitioned and a.config == "c2_kron21" and "--config" not in sys.argv:
+        a.config = "c5_kron25"
+    return a
 
 
 # ----------------------------------------------------------------- clocks sampler
@@ -192,6 +198,76 @@ def run_reference(args, rank, world):
     print(json.dumps(out), flush=True)
 
 
+# ----------------------------------------------------------------- partitioned (multi-GPU) arm
+
+def run_partitioned(args, rank, world, dev):
+    """BFS over a 1D vertex partition of one graph across all ranks (SURVEY
+    §8(e)): strong scaling (the graph is fixed, each rank owns n/P vertices).
+    Each timed step = one full BFS; time = max over ranks of the CUDA-event
+    span of the step (the level loop synchronises with the host every level)."""
+    import torch
+    import torch.distributed as dist
+
+    import graphgen as gg
+    import paper_1501_05387_b200 as gr
+    from paper_1501_05387_b200 import dist as grd
+    if world == 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+    g = gg.make_config(args.config, device=dev)
+    srcs = gg.sources(g, args.warmup + args.steps)
+    v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, world, rank)
+    deg_local = (Rl[1:] - Rl[:-1])
+    n, m = g.n, g.m
+    part = grd.GpuPartition(Rl, Cl, n, world, rank, device=dev.index)
+    del g
+    torch.cuda.empty_cache()
+    ex = grd.TorchDistExchange()
+    depth = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
+    pred = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for s in srcs[: args.warmup]:
+        grd.bfs_partitioned(part, ex, s, depth, pred)
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = gr.gr_kernel_launch_count()
+    tot_ms, edges, levels = 0.0, 0, []
+    with Clocks(dev.index) as clk:
+        for s in srcs[args.warmup:]:
+            flush.zero_()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            levels.append(grd.bfs_partitioned(part, ex, s, depth, pred))
+            e1.record()
+            torch.cuda.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot_ms += float(t[0])
+            r = torch.tensor([int(deg_local[depth >= 0].sum())], dtype=torch.int64, device=dev)
+            dist.all_reduce(r)
+            edges += int(r[0])
+    launches = gr.gr_kernel_launch_count() - launches0
+    dist.barrier()
+    value = edges / (tot_ms * 1e-3) / 1e9
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+               "config": {"workload": "%s bfs 1D-partitioned push, NCCL all-to-all per level" % args.config,
+                          "graph": CONFIG_DESC[args.config], "n": n, "m": m,
+                          "parallelism": "1D vertex partition over %d rank(s)" % world,
+                          "l2": "flushed (256 MiB write) between timed steps"},
+               "gpu_launches": launches, "levels_per_step": sum(levels) / len(levels),
+               "clocks": clk.summary(),
+               "roofline": None,
+               "e2e": None}
+        print(json.dumps(out), flush=True)
+    part.close()
+    dist.destroy_process_group()
+
+
 # ----------------------------------------------------------------- our arm
 
 def main():
@@ -213,6 +289,8 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     dev = torch.device("cuda", local)
+    if args.partitioned:
+        return run_partitioned(args, rank, world, dev)
     want_w = args.prim == "sssp"
     g = gg.make_config(args.config, device=dev, weights=want_w or None)
     G = gr.Graph(g.R, g.C, g.W if want_w else None, symmetric=True)

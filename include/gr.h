@@ -188,6 +188,58 @@ uint64_t gr_kernel_launch_count(void);
 /* Library version string, e.g. "gr_b200 0.1 sm_100a". */
 const char *gr_version(void);
 
+/* ===========================================================================
+ * Multi-GPU: 1D vertex partition (the paper is single-GPU and
+ * lists multi-GPU as future work). One process per GPU. Rank q of
+ * P owns the contiguous vertex block [q*B, min(n, (q+1)*B)), B = ceil(n/P), and
+ * stores the out-edges of its vertices with GLOBAL column ids. A BFS level is
+ *   gr_part_bfs_expand   local push advance: owned targets are claimed here,
+ *                        remote targets are culled by a per-rank "already
+ *                        sent" bitmap and bucketed per owner as
+ *                        (vertex, parent) int32 pairs;
+ *   (exchange)           the caller moves the buckets to their owners (NCCL
+ *                        all-to-all through torch.distributed, or any copy);
+ *   gr_part_bfs_absorb   the owner claims received vertices against its
+ *                        authoritative visited bitmap; survivors join its
+ *                        next local frontier;
+ *   gr_part_bfs_frontier the local next-frontier size, to be summed over
+ *                        ranks (termination when the global sum is 0).
+ * Depth / pred outputs cover the owned block only (index v - v_begin); pred
+ * holds GLOBAL parent ids.
+ * =========================================================================== */
+
+/* Creates the partition of rank `rank` out of `nparts` for a graph with
+ * n_global vertices. row_offsets int64[v_end - v_begin + 1] (local rows),
+ * col_indices int32[m_local] GLOBAL ids in [0, n_global). v_begin / v_end must
+ * equal the 1D block of `rank` (checked). Same copy / stream / error rules as
+ * gr_graph_create. */
+gr_status gr_graph_create_part(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin,
+                               int64_t v_end, int64_t m_local, const int64_t *row_offsets,
+                               const int32_t *col_indices, uint32_t flags, int device,
+                               void *cuda_stream, gr_graph **out);
+
+/* Device buffers of the exchange (valid for the graph's lifetime):
+ *   send_pairs   int32[2 * nparts * block]: bucket of peer q starts at
+ *                2 * q * block (pairs (vertex, parent), global ids)
+ *   send_counts  int64[nparts]: pairs in each bucket after gr_part_bfs_expand
+ *   recv_pairs   int32[2 * n_global]: where the caller gathers incoming pairs
+ *   block        B (vertices per partition) */
+gr_status gr_part_buffers(gr_graph *g, int32_t **send_pairs, int64_t **send_counts,
+                          int32_t **recv_pairs, int64_t *block);
+
+/* Starts a partitioned BFS from GLOBAL source src (every rank calls it).
+ * depth_out / pred_out: DEVICE int32[v_end - v_begin] (pred may be NULL),
+ * written in place by the following level calls (host memory is rejected
+ * with GR_ERR_INVALID_ARGUMENT). */
+gr_status gr_part_bfs_begin(gr_graph *g, int64_t src, int32_t *depth_out, int32_t *pred_out);
+/* Level `level` local advance; fills the send buckets and counts (device). */
+gr_status gr_part_bfs_expand(gr_graph *g, int32_t level);
+/* Claims `nrecv` received pairs (device pointer) for level `level`. */
+gr_status gr_part_bfs_absorb(gr_graph *g, int32_t level, const int32_t *recv_pairs, int64_t nrecv);
+/* Local frontier of level `level` (after expand+absorb of level-1): vertex
+ * count and edge count (host outputs). */
+gr_status gr_part_bfs_frontier(gr_graph *g, int32_t level, int64_t *f, int64_t *mf);
+
 #ifdef __cplusplus
 }
 #endif

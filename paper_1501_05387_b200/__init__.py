@@ -69,7 +69,8 @@ class gr_run_stats(ctypes.Structure):
 _lib = None
 EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
            "gr_bfs", "gr_sssp", "gr_get_run_stats", "gr_last_error", "gr_kernel_launch_count",
-           "gr_version"]
+           "gr_version", "gr_graph_create_part", "gr_part_buffers", "gr_part_bfs_begin",
+           "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier"]
 
 
 def load(path: str = LIB_PATH):
@@ -96,8 +97,18 @@ def load(path: str = LIB_PATH):
     lib.gr_last_error.restype = ctypes.c_char_p
     lib.gr_kernel_launch_count.restype = ctypes.c_uint64
     lib.gr_version.restype = ctypes.c_char_p
+    i64, i32 = ctypes.c_int64, ctypes.c_int32
+    lib.gr_graph_create_part.argtypes = [i64, i32, i32, i64, i64, i64, p, p, ctypes.c_uint32,
+                                         ctypes.c_int, p, P(p)]
+    lib.gr_part_buffers.argtypes = [p, P(p), P(p), P(p), P(i64)]
+    lib.gr_part_bfs_begin.argtypes = [p, i64, p, p]
+    lib.gr_part_bfs_expand.argtypes = [p, i32]
+    lib.gr_part_bfs_absorb.argtypes = [p, i32, p, i64]
+    lib.gr_part_bfs_frontier.argtypes = [p, i32, P(i64), P(i64)]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
-              "gr_bfs", "gr_sssp", "gr_get_run_stats"):
+              "gr_bfs", "gr_sssp", "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
+              "gr_part_bfs_begin", "gr_part_bfs_expand", "gr_part_bfs_absorb",
+              "gr_part_bfs_frontier"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib

@@ -36,7 +36,7 @@ int64_t env_int(const char *name, int64_t dflt) {
 }
 
 gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C, const uint32_t *W,
-                       uint32_t flags, int device, void *stream, Graph **out);
+                       uint32_t flags, int device, void *stream, Graph **out, int64_t ncols = -1);
 bool ptr_on_device(const void *p);
 gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr_bfs_opts &o,
                   int *launches);

@@ -111,6 +111,16 @@ struct Graph {
 
     int num_sms = 148;
     int nwords() const { return (int)((n + 31) / 32); }
+
+    // 1D partition (gr_graph_create_part); n = owned vertices, columns global
+    bool part = false;
+    int64_t n_global = 0, v_begin = 0, v_end = 0, block = 0;
+    int nparts = 1, rank = 0;
+    uint32_t *sent = nullptr;          // [ceil(n_global/32)] remote vertices already sent
+    int32_t *send_pairs = nullptr;     // [2 * nparts * block]
+    long long *send_counts = nullptr;  // [nparts]
+    int32_t *recv_pairs = nullptr;     // [2 * n_global]
+    int32_t *part_depth = nullptr, *part_pred = nullptr;
 };
 
 gr_status dev_alloc(Graph *g, void **p, size_t bytes);

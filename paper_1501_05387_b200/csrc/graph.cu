@@ -25,7 +25,8 @@ void dev_free_all(Graph *g) {
     void *ptrs[] = {g->R, g->C, g->W, (g->Rt != g->R) ? g->Rt : nullptr,
                     (g->Ct != g->C) ? g->Ct : nullptr, g->visited, g->noin, g->fbuf[0], g->fbuf[1], g->fbuf[2],
                     g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->depth_buf, g->pred_buf,
-                    g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev};
+                    g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev,
+                    g->sent, g->send_pairs, g->send_counts, g->recv_pairs};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (g->stats_host) cudaFreeHost(g->stats_host);
@@ -34,7 +35,7 @@ void dev_free_all(Graph *g) {
 // ---------------------------------------------------------------- validation
 // err[0] = first bad row-offset index (or INT64_MAX), err[1] = first bad edge.
 __global__ void validate_kernel(const int64_t *R, const int32_t *C, int64_t n, int64_t m,
-                                unsigned long long *err) {
+                                int64_t ncols, unsigned long long *err) {
     int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     int64_t nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = tid; i <= n; i += nt) {
@@ -44,7 +45,7 @@ __global__ void validate_kernel(const int64_t *R, const int32_t *C, int64_t n, i
     }
     for (int64_t e = tid; e < m; e += nt) {
         int32_t c = C[e];
-        if (c < 0 || c >= n) atomicMin(err + 1, (unsigned long long)e);
+        if (c < 0 || c >= ncols) atomicMin(err + 1, (unsigned long long)e);
     }
 }
 
@@ -127,10 +128,12 @@ static int bits_for(int64_t x) {  // smallest S with x < 2^S
 }
 
 gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C, const uint32_t *W,
-                       uint32_t flags, int device, void *stream, Graph **out) {
+                       uint32_t flags, int device, void *stream, Graph **out, int64_t ncols) {
     if (!out) { set_error("out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     *out = nullptr;
     if (n <= 0 || n > 0x7fffffffLL) { set_error("n=%lld must be in [1, 2^31-1]", (long long)n); return GR_ERR_INVALID_ARGUMENT; }
+    if (ncols < 0) ncols = n;  // partitions: columns are global ids in [0, n_global)
+    if (ncols != n) flags |= GR_SYMMETRIC;  // no CSC for a partition (push only)
     if (m < 0) { set_error("m=%lld < 0", (long long)m); return GR_ERR_INVALID_ARGUMENT; }
     if (!R || (m > 0 && !C)) { set_error("row_offsets / col_indices is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     GR_CUDA(cudaSetDevice(device));
@@ -162,7 +165,7 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
     if (flags & GR_VALIDATE) {
         unsigned long long init[2] = {~0ull, ~0ull}, res[2];
         TRYC(cudaMemcpyAsync(tmp, init, sizeof(init), cudaMemcpyHostToDevice, s));
-        validate_kernel<<<blocks, 256, 0, s>>>(g->R, g->C, n, m, tmp);
+        validate_kernel<<<blocks, 256, 0, s>>>(g->R, g->C, n, m, ncols, tmp);
         count_launch();
         TRYC(cudaMemcpyAsync(res, tmp, sizeof(res), cudaMemcpyDeviceToHost, s));
         TRYC(cudaStreamSynchronize(s));
@@ -178,7 +181,7 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
             } else {
                 int32_t c;
                 TRYC(cudaMemcpy(&c, g->C + res[1], sizeof(int32_t), cudaMemcpyDeviceToHost));
-                set_error("C[%llu]=%d not in [0, n=%lld)", res[1], c, (long long)n);
+                set_error("C[%llu]=%d not in [0, n=%lld)", res[1], c, (long long)ncols);
             }
             cudaFree(tmp);
             dev_free_all(g);
