@@ -60,6 +60,8 @@ struct BfsArgs {
     int64_t nonisolated;
     int S;
     int64_t small_f, small_e;  // small-mode thresholds (<= kSmallF, tuning knobs)
+    int32_t strategy;          // 0 auto, 1 thread/warp/CTA, 2 merge-path (gr_bfs_opts)
+    int64_t lb_threshold;      // auto: frontiers below it use thread/warp/CTA
 };
 
 struct BfsSmem {
@@ -81,6 +83,7 @@ struct BfsSmem {
     unsigned long long pk[3];   // small mode: packed (edges << kSmallCntBits) | count, per level mod 3
     unsigned long long nd[3];   // small mode: discovered per level mod 3
     int work;
+    int win;     // expand_twc: CTA arbitration
 };
 
 // ---------------------------------------------------------------------------
@@ -608,11 +611,22 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                          a.idempotent, &app, 0ull, pol_keep,
                          mf < (1 << 16) ? 0 : (st.m_u * 4 < a.m ? 2 : 1)};
             GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.R, f, mf};
+            // auto (reading A-4, measured on B200): node-granular thread/warp/CTA
+            // when the frontier's lists are short on average (mesh-like levels:
+            // no frontier-wide search, 35% faster per level on C4); merge-path
+            // over edges when a few lists carry the edges (hubs: one CTA per list
+            // would serialise them; C2 level 1 is 26% slower with TWC)
+            const bool twc = a.strategy == 1 ||
+                             (a.strategy == 0 && f < a.lb_threshold && mf <= 16 * f);
+            if (twc) {
+                expand_twc(fr, a.C, op, &s->win);
+            } else {
 #if GR_BFS_STAGES > 0
             expand_pipe<kBfsStages, false>(fr, a.C, nullptr, gw, nw, op, &s->u.stage.pipe[wib]);
 #else
             expand_lb(fr, a.C, gw, nw, op);
 #endif
+            }
             ndisc = op.ndisc;
             st.fb_valid = st.fbn_clean;
         } else {
@@ -660,6 +674,8 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.direction = o.direction;
     a.switch_rule = o.switch_rule;
     a.idempotent = o.idempotent;
+    a.strategy = o.strategy;
+    a.lb_threshold = o.lb_threshold > 0 ? o.lb_threshold : env_int("GR_LB_THRESHOLD", 1ll << 40);
     a.alpha = o.alpha > 0 ? o.alpha : 14.0;
     a.beta = o.beta > 0 ? o.beta : 24.0;
     a.nonisolated = g->nonisolated;

@@ -229,6 +229,7 @@ struct SmemFrontier {
 //   void edges<U>(ok[], src[], pay[], dst[], eidx[])  process U edges per lane
 // ---------------------------------------------------------------------------
 constexpr int kUnroll = 4;
+constexpr int kGroup = 32 * kUnroll;          // edges per warp group
 
 template <class Front, class Op>
 __device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__restrict__ C, int64_t gw,
@@ -322,6 +323,131 @@ __device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__rest
 }
 
 // ---------------------------------------------------------------------------
+// Node-granular thread/warp/CTA advance ("per-warp and per-CTA coarse-grained"
+// mapping of Merrill et al., with the fine-grained per-thread class
+// of P:693-706). Each CTA takes a contiguous slice of the frontier, one vertex
+// per thread per round; lists are classified by size:
+//   large  (> blockDim edges): threads arbitrate for the whole CTA, which
+//          sweeps the winner's list (coalesced);
+//   medium (> 32 edges):       lanes arbitrate for their warp;
+//   small  (<= 32 edges):      the warp concatenates its small lists (warp
+//          scan of degrees) and maps each edge to its owner with the 5-step
+//          shuffle search, i.e. per-thread work balanced inside the warp.
+// No frontier-wide prefix or search is needed (node-granular balancing; the
+// paper selects it for frontiers below the 4096 threshold).
+// All threads of the CTA must call it (CTA barriers inside).
+// ---------------------------------------------------------------------------
+template <class Front, class Op>
+__device__ __forceinline__ void expand_twc(const Front &fr, const int32_t *__restrict__ C, Op &op,
+                                           int *s_win) {
+    const int64_t F = fr.F;
+    const int64_t j0 = F * blockIdx.x / gridDim.x, j1 = F * (blockIdx.x + 1) / gridDim.x;
+    const unsigned l = lane_id();
+    const int wib = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+    const unsigned long long pol = policy_evict_first();
+    for (int64_t base = j0; base < j1; base += blockDim.x) {  // uniform trip count in the CTA
+        const int64_t j = base + threadIdx.x;
+        int32_t v = 0;
+        int64_t o = 0, rs = 0, end = 0;
+        if (j < j1) fr.load(j, v, o, rs, end);
+        int64_t deg = end - o;
+        const unsigned long long pay = (j < j1) ? op.entry(v) : 0ull;
+        // ---- large lists: the whole CTA ---------------------------------------
+        for (;;) {
+            if (threadIdx.x == 0) *s_win = -1;
+            __syncthreads();
+            if (deg > (int64_t)blockDim.x) atomicMax(s_win, (int)threadIdx.x);
+            __syncthreads();
+            const int win = *s_win;
+            __syncthreads();
+            if (win < 0) break;
+            // broadcast the winner's list through shared memory
+            __shared__ long long s_list[3];
+            if ((int)threadIdx.x == win) { s_list[0] = rs; s_list[1] = deg; s_list[2] = ((long long)v << 32) | (unsigned)pay; deg = 0; }
+            __syncthreads();
+            const int64_t lrs = s_list[0], ldeg = s_list[1];
+            const int32_t lv = (int32_t)(s_list[2] >> 32);
+            const unsigned long long lpay = (unsigned)(s_list[2] & 0xffffffffu);
+            __syncthreads();
+            for (int64_t x = (int64_t)wib * kGroup; x < ldeg; x += (int64_t)nwb * kGroup) {
+                bool ok[kUnroll];
+                int32_t src[kUnroll], dst[kUnroll];
+                unsigned long long sp[kUnroll];
+                int64_t eidx[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int64_t k = x + u * 32 + l;
+                    ok[u] = k < ldeg;
+                    src[u] = lv;
+                    sp[u] = lpay;
+                    eidx[u] = lrs + k;
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) dst[u] = ok[u] ? ld_stream(C + eidx[u], pol) : 0;
+                op.template edges<kUnroll>(ok, src, sp, dst, eidx);
+            }
+        }
+        // ---- medium lists: the warp ----------------------------------------------
+        for (;;) {
+            const unsigned med = __ballot_sync(0xffffffffu, deg > 32);
+            if (!med) break;
+            const int ldr = __ffs(med) - 1;
+            const int64_t lrs = __shfl_sync(0xffffffffu, rs, ldr);
+            const int64_t ldeg = __shfl_sync(0xffffffffu, deg, ldr);
+            const int32_t lv = __shfl_sync(0xffffffffu, v, ldr);
+            const unsigned long long lpay = __shfl_sync(0xffffffffu, pay, ldr);
+            if ((int)l == ldr) deg = 0;
+            for (int64_t x = 0; x < ldeg; x += kGroup) {
+                bool ok[kUnroll];
+                int32_t src[kUnroll], dst[kUnroll];
+                unsigned long long sp[kUnroll];
+                int64_t eidx[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    const int64_t k = x + u * 32 + l;
+                    ok[u] = k < ldeg;
+                    src[u] = lv;
+                    sp[u] = lpay;
+                    eidx[u] = lrs + k;
+                }
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) dst[u] = ok[u] ? ld_stream(C + eidx[u], pol) : 0;
+                op.template edges<kUnroll>(ok, src, sp, dst, eidx);
+            }
+        }
+        // ---- small lists: warp-level concatenation ---------------------------
+        const int32_t d32 = (int32_t)deg;  // <= 32
+        const int32_t incl = warp_incl_scan<int32_t>(d32);
+        const int32_t excl = incl - d32;
+        const int32_t T = __shfl_sync(0xffffffffu, incl, 31);
+        const int64_t shift = rs - excl;
+        for (int32_t x = 0; x < T; x += kGroup) {
+            bool ok[kUnroll];
+            int32_t src[kUnroll], dst[kUnroll];
+            unsigned long long sp[kUnroll];
+            int64_t eidx[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int32_t my = x + u * 32 + (int32_t)l;
+                int k = 0;
+#pragma unroll
+                for (int st = 16; st >= 1; st >>= 1) {
+                    const int32_t oc = __shfl_sync(0xffffffffu, excl, k + st);
+                    if (oc <= my) k += st;
+                }
+                ok[u] = my < T;
+                src[u] = __shfl_sync(0xffffffffu, v, k);
+                sp[u] = __shfl_sync(0xffffffffu, pay, k);
+                eidx[u] = my + __shfl_sync(0xffffffffu, shift, k);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) dst[u] = ok[u] ? ld_stream(C + eidx[u], pol) : 0;
+            op.template edges<kUnroll>(ok, src, sp, dst, eidx);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Pipelined load-balanced advance (grid levels). Same merge-path partition
 // and owner mapping as expand_lb, but the neighbour ids (and weights) of the
 // next kStages groups of 128 edges are copied global -> shared memory with
@@ -331,7 +457,6 @@ __device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__rest
 // most edges of a power-law graph) is copied as 16-byte chunks of the aligned
 // superset of its range; a mixed group element by element.
 // ---------------------------------------------------------------------------
-constexpr int kGroup = 32 * kUnroll;          // edges per group
 constexpr int kGroupBuf = kGroup + 8;         // aligned superset (16-byte chunks)
 
 struct PipeStageMeta {

@@ -239,3 +239,16 @@ def test_run_stats_levels(gr):
         want = int(((ref == L) & (deg > 0)).sum())
         assert rec["frontier"] == want
         assert rec["frontier_edges"] == int(deg[ref == L].sum())
+
+
+@pytest.mark.parametrize("strategy", ["twc", "lb"])
+def test_strategies_forced(gr, strategy):
+    """Thread/warp/CTA and merge-path advances give the
+    same depths on skewed (hub lists > CTA size), directed and mesh graphs."""
+    for g in (gg.rmat(14, 16, seed=2), gg.star(200_000), gg.directed_random(40000, 300000, seed=4),
+              gg.make_config("c4_road", shrink=4)):
+        g = gg.assign_weights(g, seed=1)
+        G = _dev(g, gr)
+        srcs = gg.sources(g, 2)
+        _check_bfs(gr, G, g, srcs, dirs=["push", "auto"], strategy=strategy)
+        _check_bfs(gr, G, g, srcs[:1], dirs=["push"], strategy=strategy, idempotent=True)
