@@ -186,7 +186,9 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
         // bands (fewer bulk-synchronous iterations).
         double avg = g->n ? (double)g->m / (double)g->n : 0.0;
         uint64_t mw = g->max_w ? g->max_w : 1;
-        delta = avg >= 8.0 ? (mw + 7) / 8 : mw * 16;
+        // swept on B200: C3 (avg deg 76, w<=64) best at 3 of {1,2,3,4,8,16,32};
+        // C4 (avg deg 2.4) best at 2048 of {256..16384}
+        delta = avg >= 8.0 ? (mw + 10) / 21 : mw * 32;
         if (delta == 0) delta = 1;
     }
     GR_CUDA(cudaSetDevice(g->device));

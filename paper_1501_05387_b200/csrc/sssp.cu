@@ -43,6 +43,7 @@ struct SsspSmem {
     int32_t fv[kWarpsPerBlock][kSsspStage];   // far staging
     unsigned long long ctl[8];
     unsigned long long bsum[4];
+    int win;  // expand_twc: CTA arbitration
 };
 
 // Fused advance + compute + filter of one near iteration (a10).
@@ -62,13 +63,19 @@ struct RelaxOp {
         return ld_probe(dp + v, pol_keep) >> 32;  // dist[u] read when the window is loaded
     }
 
-    // w[]: the edge weights, staged in shared memory by the pipelined advance
-    template <int U>
+    // x[]: the edge weights staged in shared memory by the pipelined advance
+    // (uint32), or the edge indices (int64) from expand_lb / expand_twc
+    template <int U, class T5>
     __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *du,
-                                          const int32_t *dst, const uint32_t *w) {
+                                          const int32_t *dst, const T5 *x) {
         unsigned long long cur[U];
+        uint32_t w[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) cur[u] = ok[u] ? ld_probe(dp + dst[u], pol_keep) : 0ull;
+        for (int u = 0; u < U; ++u) {
+            if constexpr (sizeof(T5) == 8) w[u] = ok[u] ? __ldg(W + x[u]) : 0u;
+            else w[u] = (uint32_t)x[u];
+            cur[u] = ok[u] ? ld_probe(dp + dst[u], pol_keep) : 0ull;
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             bool to_near = false, to_far = false;
@@ -195,7 +202,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             farq.counter = &a.ctl->far_count[fp];
             RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.R, f, mf};
-            expand_pipe<kSsspStages, true>(fr, a.C, a.W, gw, nw, op, &s->pipe[wib]);
+            // same auto rule as BFS (reading A-4): short lists -> thread/warp/CTA
+            if (mf <= 16 * f)
+                expand_twc(fr, a.C, op, &s->win);
+            else
+                expand_pipe<kSsspStages, true>(fr, a.C, a.W, gw, nw, op, &s->pipe[wib]);
             nearq.finish();
             farq.finish();
             const unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
