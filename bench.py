@@ -255,7 +255,9 @@ def run_partitioned(args, rank, world, dev):
         out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
                "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-               "config": {"workload": "%s bfs 1D-partitioned push, NCCL all-to-all per level" % args.config,
+               "config": {"workload": "%s bfs 1D-partitioned direction-optimizing: push levels "
+                                      "NCCL all-to-all of (vertex,parent), pull levels NCCL all-gather "
+                                      "of the frontier bitmap" % args.config,
                           "graph": CONFIG_DESC[args.config], "n": n, "m": m,
                           "parallelism": "1D vertex partition over %d rank(s)" % world,
                           "l2": "flushed (256 MiB write) between timed steps"},

@@ -191,7 +191,8 @@ const char *gr_version(void);
 /* ===========================================================================
  * Multi-GPU: 1D vertex partition (the paper is single-GPU and
  * lists multi-GPU as future work). One process per GPU. Rank q of
- * P owns the contiguous vertex block [q*B, min(n, (q+1)*B)), B = ceil(n/P), and
+ * P owns the contiguous vertex block [q*B, min(n, (q+1)*B)), B = 32*ceil(n/(32P))
+ * (word-aligned so frontier-bitmap shards concatenate), and
  * stores the out-edges of its vertices with GLOBAL column ids. A BFS level is
  *   gr_part_bfs_expand   local push advance: owned targets are claimed here,
  *                        remote targets are culled by a per-rank "already
@@ -239,6 +240,20 @@ gr_status gr_part_bfs_absorb(gr_graph *g, int32_t level, const int32_t *recv_pai
 /* Local frontier of level `level` (after expand+absorb of level-1): vertex
  * count and edge count (host outputs). */
 gr_status gr_part_bfs_frontier(gr_graph *g, int32_t level, int64_t *f, int64_t *mf);
+
+/* Dense (pull) levels of a partitioned BFS, for
+ * symmetric graphs (out-lists double as in-lists):
+ *   gr_part_bfs_shard  writes this rank's slice of the frontier bitmap of
+ *                      `level` (block/32 words, bit i = vertex v_begin + i)
+ *                      into `shard` (device);
+ *   (all-gather)       the caller concatenates the shards of all ranks in
+ *                      rank order into a global bitmap of nparts*block bits;
+ *   gr_part_bfs_pull   bottom-up step over the owned unvisited vertices
+ *                      against that global bitmap; builds the local frontier
+ *                      of level+1 (no exchange needed: parents are global ids).
+ * block is a multiple of 32 (block = 32*ceil(n/(32*nparts))). */
+gr_status gr_part_bfs_shard(gr_graph *g, int32_t level, uint32_t *shard);
+gr_status gr_part_bfs_pull(gr_graph *g, int32_t level, const uint32_t *global_frontier);
 
 #ifdef __cplusplus
 }

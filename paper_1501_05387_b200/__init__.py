@@ -70,7 +70,8 @@ _lib = None
 EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
            "gr_bfs", "gr_sssp", "gr_get_run_stats", "gr_last_error", "gr_kernel_launch_count",
            "gr_version", "gr_graph_create_part", "gr_part_buffers", "gr_part_bfs_begin",
-           "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier"]
+           "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_shard",
+           "gr_part_bfs_pull"]
 
 
 def load(path: str = LIB_PATH):
@@ -105,10 +106,12 @@ def load(path: str = LIB_PATH):
     lib.gr_part_bfs_expand.argtypes = [p, i32]
     lib.gr_part_bfs_absorb.argtypes = [p, i32, p, i64]
     lib.gr_part_bfs_frontier.argtypes = [p, i32, P(i64), P(i64)]
+    lib.gr_part_bfs_shard.argtypes = [p, i32, p]
+    lib.gr_part_bfs_pull.argtypes = [p, i32, p]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
               "gr_bfs", "gr_sssp", "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
               "gr_part_bfs_begin", "gr_part_bfs_expand", "gr_part_bfs_absorb",
-              "gr_part_bfs_frontier"):
+              "gr_part_bfs_frontier", "gr_part_bfs_shard", "gr_part_bfs_pull"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib

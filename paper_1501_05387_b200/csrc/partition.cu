@@ -182,6 +182,78 @@ __global__ void __launch_bounds__(kPartBlock) part_absorb_kernel(PartArgs a, int
     app.finish();
 }
 
+// frontier bitmap shard of level `level` from the local queue
+__global__ void part_shard_clear_kernel(uint32_t *shard, int64_t words) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t w = tid; w < words; w += nt) shard[w] = 0u;
+}
+__global__ void part_shard_fill_kernel(PartArgs a, int level, uint32_t *shard) {
+    const unsigned long long qp = ld_relaxed(&a.ctl->slot[level & 3].qpack);
+    const int64_t f = (int64_t)(qp & ((1ull << a.S) - 1));
+    const int32_t *q = a.qv[level & 1];
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = tid; j < f; j += nt) {
+        const int32_t v = q[j];
+        atomicOr(shard + (v >> 5), 1u << (v & 31));
+    }
+}
+
+// Bottom-up step of a partition: owned unvisited vertices look for
+// a parent in the GLOBAL frontier bitmap; a warp owns one 32-vertex word of the
+// local visited bitmap (ballot + store, no atomics); discovered vertices join
+// the local queue of level + 1 (merge-path prefix via the packed counter).
+__global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int level, const uint32_t *gfront) {
+    __shared__ int32_t s_v[kPartWarps][kPartStage];
+    __shared__ int32_t s_d[kPartWarps][kPartStage];
+    const int wib = threadIdx.x >> 5;
+    const unsigned l = lane_id();
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        Slot &r = a.ctl->slot[(level + 2) & 3];
+        r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull;
+    }
+    PartAppender app;
+    app.sv = s_v[wib]; app.sd = s_d[wib]; app.cnt = 0; app.S = a.S; app.cap = a.n_local;
+    app.overflow = &a.ctl->overflow;
+    app.qv = a.qv[(level + 1) & 1];
+    app.qo = a.qo[(level + 1) & 1];
+    app.counter = &a.ctl->slot[(level + 1) & 3].qpack;
+    const unsigned long long pol = policy_evict_first();
+    const int64_t nwords = (a.n_local + 31) / 32;
+    for (int64_t wi = gw; wi < nwords; wi += nw) {
+        const int64_t v = wi * 32 + l;
+        const uint32_t visw = a.visited[wi];
+        bool found = false;
+        int32_t parent = -1;
+        int64_t beg = 0, end = 0;
+        if (v < a.n_local && !((visw >> l) & 1u)) { beg = a.R[v]; end = a.R[v + 1]; }
+        for (int64_t e = beg; e < end && !found; e += 4) {
+            int32_t u[4];
+            uint32_t fw[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) u[k] = (e + k < end) ? ld_stream(a.C + e + k, pol) : -1;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) fw[k] = (u[k] >= 0) ? __ldg(gfront + (u[k] >> 5)) : 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (!found && u[k] >= 0 && ((fw[k] >> (u[k] & 31)) & 1u)) { found = true; parent = u[k]; }
+        }
+        const unsigned nb = __ballot_sync(0xffffffffu, found);
+        if (l == 0 && nb) a.visited[wi] = visw | nb;
+        int64_t deg = 0;
+        if (found) {
+            a.depth[v] = level + 1;
+            if (a.pred) a.pred[v] = parent;
+            deg = end - beg;
+        }
+        app.push(found && deg > 0, (int32_t)v, deg);
+    }
+    app.finish();
+}
+
 static PartArgs part_args(Graph *g) {
     PartArgs a;
     a.n_local = g->n; a.v_begin = g->v_begin; a.block = g->block; a.nparts = g->nparts;
@@ -207,7 +279,7 @@ gr_status gr_graph_create_part(int64_t n_global, int32_t nparts, int32_t rank, i
         set_error("invalid partition arguments (nparts=%d rank=%d n_global=%lld)", nparts, rank, (long long)n_global);
         return GR_ERR_INVALID_ARGUMENT;
     }
-    const int64_t block = (n_global + nparts - 1) / nparts;
+    const int64_t block = 32 * ((n_global + 32 * (int64_t)nparts - 1) / (32 * (int64_t)nparts));
     const int64_t vb = (int64_t)rank * block, ve = vb + block < n_global ? vb + block : n_global;
     if (v_begin != vb || v_end != ve || ve <= vb) {
         set_error("rank %d of %d must own [%lld, %lld), got [%lld, %lld)", rank, nparts, (long long)vb,
@@ -288,6 +360,27 @@ gr_status gr_part_bfs_absorb(gr_graph *h, int32_t level, const int32_t *recv_pai
     const int64_t blocks = (nrecv + kPartBlock - 1) / kPartBlock;
     part_absorb_kernel<<<(int)(blocks < g->num_sms * 8 ? blocks : g->num_sms * 8), kPartBlock, 0, g->stream>>>(
         a, level, recv_pairs, nrecv);
+    count_launch();
+    GR_CUDA(cudaGetLastError());
+    return GR_OK;
+}
+
+gr_status gr_part_bfs_shard(gr_graph *h, int32_t level, uint32_t *shard) {
+    Graph *g = (Graph *)h;
+    if (!g || !g->part || level < 0 || !shard) { set_error("invalid argument"); return GR_ERR_INVALID_ARGUMENT; }
+    PartArgs a = part_args(g);
+    part_shard_clear_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(shard, g->block / 32);
+    part_shard_fill_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(a, level, shard);
+    count_launch(2);
+    GR_CUDA(cudaGetLastError());
+    return GR_OK;
+}
+
+gr_status gr_part_bfs_pull(gr_graph *h, int32_t level, const uint32_t *global_frontier) {
+    Graph *g = (Graph *)h;
+    if (!g || !g->part || level < 0 || !global_frontier) { set_error("invalid argument"); return GR_ERR_INVALID_ARGUMENT; }
+    PartArgs a = part_args(g);
+    part_pull_kernel<<<g->num_sms * 8, kPartBlock, 0, g->stream>>>(a, level, global_frontier);
     count_launch();
     GR_CUDA(cudaGetLastError());
     return GR_OK;

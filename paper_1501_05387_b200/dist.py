@@ -34,7 +34,8 @@ GR_VALIDATE = 4
 
 
 def block_size(n: int, nparts: int) -> int:
-    return (n + nparts - 1) // nparts
+    """Vertices per partition, a multiple of 32 (bitmap shards concatenate)."""
+    return 32 * ((n + 32 * nparts - 1) // (32 * nparts))
 
 
 def owned_range(n: int, nparts: int, rank: int):
@@ -63,7 +64,8 @@ class GpuPartition:
     """The partition of this rank on one GPU (C ABI gr_graph_create_part)."""
 
     def __init__(self, R_local, C_local, n_global: int, nparts: int, rank: int, device: int = None,
-                 stream=None, validate: bool = True):
+                 stream=None, validate: bool = True, symmetric: bool = True):
+        self.symmetric = symmetric
         if device is None:
             device = torch.cuda.current_device()
         self.device = device
@@ -89,6 +91,13 @@ class GpuPartition:
         self.send_pairs = torch.as_tensor(_CudaArray(sp.value, 2 * nparts * self.block, "<i4", device), device=dev)
         self.send_counts = torch.as_tensor(_CudaArray(sc.value, nparts, "<i8", device), device=dev)
         self.recv_pairs = torch.as_tensor(_CudaArray(rv.value, 2 * n_global, "<i4", device), device=dev)
+        # dense levels: this rank's frontier-bitmap shard and the gathered global bitmap
+        self.shard_buf = torch.zeros(self.block // 32, dtype=torch.int32, device=dev)
+        self.global_buf = torch.zeros(nparts * self.block // 32, dtype=torch.int32, device=dev)
+        deg = R_local[1:] - R_local[:-1]
+        self.nonisolated_local = int((deg > 0).sum())
+        self.m_local = int(C_local.numel())
+        self._deg = deg
 
     def close(self):
         if getattr(self, "handle", None) is not None:
@@ -117,6 +126,19 @@ class GpuPartition:
         _check(load().gr_part_bfs_frontier(self.handle, level, ctypes.byref(f), ctypes.byref(mf)))
         return f.value, mf.value
 
+    def degree(self, v_global: int) -> int:
+        """Out-degree of an owned vertex (0 if not owned)."""
+        if self.v_begin <= v_global < self.v_end:
+            return int(self._deg[v_global - self.v_begin])
+        return 0
+
+    def shard(self, level: int) -> torch.Tensor:
+        _check(load().gr_part_bfs_shard(self.handle, level, self.shard_buf.data_ptr()))
+        return self.shard_buf
+
+    def pull(self, level: int, global_bits: torch.Tensor):
+        _check(load().gr_part_bfs_pull(self.handle, level, global_bits.data_ptr()))
+
 
 class TorchDistExchange:
     """Exchange over a torch.distributed process group (NCCL or gloo)."""
@@ -142,6 +164,14 @@ class TorchDistExchange:
         self.dist.all_reduce(x, group=self.group)
         return x
 
+    def allgather(self, shard: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        try:
+            self.dist.all_gather_into_tensor(out, shard, group=self.group)
+        except (RuntimeError, NotImplementedError):  # backends without the fused variant
+            parts = list(out.chunk(self.dist.get_world_size(self.group)))
+            self.dist.all_gather(parts, shard, group=self.group)
+        return out
+
 
 def _gather_buckets(part, send_counts_host: Sequence[int]):
     """Concatenate the used part of every peer bucket (pairs, flat int32)."""
@@ -150,28 +180,61 @@ def _gather_buckets(part, send_counts_host: Sequence[int]):
     return torch.cat(pieces) if pieces else part.send_pairs[:0]
 
 
+def decide_direction(direction: str, cur: str, f: int, mf: int, u: int, m_u: int, prev_f: int,
+                     n: int, nonisolated: int, alpha: float = 14.0, beta: float = 24.0) -> str:
+    """Beamer's rule on GLOBAL counters (reading A-3; same rule as the
+    single-GPU kernel): push->pull when m_f > m_u/alpha and m_f >= n/32,
+    pull->push when f < nonisolated/beta and the frontier shrinks."""
+    if direction in ("push", "pull"):
+        return direction
+    if cur == "push":
+        return "pull" if (mf > m_u / alpha and mf >= (n + 31) // 32) else "push"
+    return "push" if (f < nonisolated / beta and f < prev_f) else "pull"
+
+
 def bfs_partitioned(part, exchange, src: int, depth: torch.Tensor, pred: torch.Tensor = None,
-                    max_levels: int = 1 << 30):
-    """Runs one BFS over the partition of this rank. Returns the number of levels."""
+                    direction: str = "auto", max_levels: int = 1 << 30, trace: list = None):
+    """Runs one BFS over the partition of this rank (all ranks call it with the
+    same arguments). Sparse levels push + all-to-all; dense levels all-gather
+    the frontier bitmap and pull. Returns the number of levels."""
     dev = depth.device
     part.begin(src, depth, pred)
-    f, _ = part.frontier(0)
-    tot = exchange.allreduce_sum(torch.tensor([f], dtype=torch.int64, device=dev))
-    level = 0
-    while int(tot[0]) > 0 and level < max_levels:
-        part.expand(level)
-        sc = part.send_counts.clone() if part.send_counts.device == dev else part.send_counts.to(dev)
-        rc = exchange.counts(sc)
-        sc_h = sc.tolist()
-        rc_h = rc.tolist()
-        send_flat = _gather_buckets(part, sc_h)
-        nrecv = int(sum(rc_h))
-        out = part.recv_pairs[: 2 * nrecv]
-        exchange.pairs(send_flat, out, [2 * c for c in sc_h], [2 * c for c in rc_h])
-        part.absorb(level, out, nrecv)
+    dsrc = part.degree(src)
+    f, mf = part.frontier(0)
+    init = torch.tensor([f, mf, part.nonisolated_local - (1 if dsrc > 0 else 0), part.m_local - dsrc,
+                         part.nonisolated_local], dtype=torch.int64, device=dev)
+    init = exchange.allreduce_sum(init).tolist()
+    f, mf, u, m_u, nonisolated = init
+    n = part.n_global
+    level, cur, prev_f = 0, "push", 0
+    if not getattr(part, "symmetric", True):
+        direction = "push"  # pull reads out-lists as in-lists: symmetric graphs only
+    while f > 0 and level < max_levels:
+        cur = decide_direction(direction, cur, f, mf, u, m_u, prev_f, n, nonisolated)
+        if trace is not None:
+            trace.append((level, cur, f, mf))
+        if cur == "push":
+            part.expand(level)
+            sc = part.send_counts.clone() if part.send_counts.device == dev else part.send_counts.to(dev)
+            rc = exchange.counts(sc)
+            sc_h = sc.tolist()
+            rc_h = rc.tolist()
+            send_flat = _gather_buckets(part, sc_h)
+            nrecv = int(sum(rc_h))
+            out = part.recv_pairs[: 2 * nrecv]
+            exchange.pairs(send_flat, out, [2 * c for c in sc_h], [2 * c for c in rc_h])
+            part.absorb(level, out, nrecv)
+        else:
+            shard = part.shard(level)
+            exchange.allgather(shard, part.global_buf)
+            part.pull(level, part.global_buf)
         level += 1
-        f, _ = part.frontier(level)
-        tot = exchange.allreduce_sum(torch.tensor([f], dtype=torch.int64, device=dev))
+        prev_f = f
+        lf, lmf = part.frontier(level)
+        tot = exchange.allreduce_sum(torch.tensor([lf, lmf], dtype=torch.int64, device=dev)).tolist()
+        f, mf = tot
+        u -= f  # symmetric graphs: every discovered vertex has out-degree > 0
+        m_u -= mf
     return level
 
 
@@ -182,27 +245,45 @@ class LoopbackGroup:
     def __init__(self, parts):
         self.parts = parts
 
-    def bfs(self, src: int, depths, preds):
+    def bfs(self, src: int, depths, preds, direction: str = "auto"):
         P = len(self.parts)
-        dev = depths[0].device
         for q, pt in enumerate(self.parts):
             pt.begin(src, depths[q], preds[q] if preds else None)
-        level = 0
-        tot = sum(pt.frontier(0)[0] for pt in self.parts)
-        while tot > 0:
-            for pt in self.parts:
-                pt.expand(level)
-            counts = [pt.send_counts.tolist() for pt in self.parts]  # counts[src_rank][dst_rank]
-            for dst in range(P):
-                pieces = []
-                for s in range(P):
-                    c = counts[s][dst]
-                    B = self.parts[s].block
-                    pieces.append(self.parts[s].send_pairs[2 * dst * B: 2 * dst * B + 2 * c])
-                flat = torch.cat(pieces)
-                n = flat.numel() // 2
-                self.parts[dst].recv_pairs[: flat.numel()].copy_(flat)
-                self.parts[dst].absorb(level, self.parts[dst].recv_pairs, n)
+        dsrc = sum(pt.degree(src) for pt in self.parts)
+        f = sum(pt.frontier(0)[0] for pt in self.parts)
+        mf = sum(pt.frontier(0)[1] for pt in self.parts)
+        nonisolated = sum(pt.nonisolated_local for pt in self.parts)
+        u = nonisolated - (1 if dsrc > 0 else 0)
+        m_u = sum(pt.m_local for pt in self.parts) - dsrc
+        n = self.parts[0].n_global
+        level, cur, prev_f = 0, "push", 0
+        self.dirs = []
+        if not all(getattr(pt, "symmetric", True) for pt in self.parts):
+            direction = "push"
+        while f > 0:
+            cur = decide_direction(direction, cur, f, mf, u, m_u, prev_f, n, nonisolated)
+            self.dirs.append(cur)
+            if cur == "push":
+                for pt in self.parts:
+                    pt.expand(level)
+                counts = [pt.send_counts.tolist() for pt in self.parts]  # counts[src_rank][dst_rank]
+                for dst in range(P):
+                    pieces = []
+                    for s in range(P):
+                        c = counts[s][dst]
+                        B = self.parts[s].block
+                        pieces.append(self.parts[s].send_pairs[2 * dst * B: 2 * dst * B + 2 * c])
+                    flat = torch.cat(pieces)
+                    self.parts[dst].recv_pairs[: flat.numel()].copy_(flat)
+                    self.parts[dst].absorb(level, self.parts[dst].recv_pairs, flat.numel() // 2)
+            else:
+                gathered = torch.cat([pt.shard(level).clone() for pt in self.parts])
+                for pt in self.parts:
+                    pt.pull(level, gathered)
             level += 1
-            tot = sum(pt.frontier(level)[0] for pt in self.parts)
+            prev_f = f
+            f = sum(pt.frontier(level)[0] for pt in self.parts)
+            mf = sum(pt.frontier(level)[1] for pt in self.parts)
+            u -= f
+            m_u -= mf
         return level

@@ -32,6 +32,34 @@ class PartitionDouble:
         self.send_pairs = torch.zeros(2 * nparts * self.block, dtype=torch.int32)
         self.send_counts = torch.zeros(nparts, dtype=torch.int64)
         self.recv_pairs = torch.zeros(2 * n_global, dtype=torch.int32)
+        self.global_buf = torch.zeros(nparts * self.block // 32, dtype=torch.int32)
+        deg = np.diff(self.R)
+        self.nonisolated_local = int((deg > 0).sum())
+        self.m_local = int(self.C.size)
+
+    def degree(self, v):
+        return int(self.R[v - self.v_begin + 1] - self.R[v - self.v_begin]) if self.v_begin <= v < self.v_end else 0
+
+    def shard(self, level):
+        bits = np.zeros(self.block // 32, np.uint32)
+        for v in self.queues.get(level, []):
+            bits[v >> 5] |= np.uint32(1 << (v & 31))
+        return torch.from_numpy(bits.view(np.int32))
+
+    def pull(self, level, global_bits):
+        g = global_bits.numpy().view(np.uint32)
+        nxt = self.queues.setdefault(level + 1, [])
+        for v in range(self.n_local):
+            if self.visited[v]:
+                continue
+            for e in range(self.R[v], self.R[v + 1]):
+                u = int(self.C[e])
+                if (g[u >> 5] >> (u & 31)) & 1:
+                    self.visited[v] = True
+                    self.depth[v] = level + 1
+                    self.pred[v] = u
+                    nxt.append(v)
+                    break
 
     def begin(self, src, depth, pred):
         self.depth, self.pred = depth, pred
@@ -97,13 +125,17 @@ def _worker(rank, world, port, graph_name, srcs, out):
         g = _graph(graph_name)
         v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, world, rank)
         part = PartitionDouble(Rl, Cl, g.n, world, rank)
+        part.symmetric = g.symmetric
         ex = grd.TorchDistExchange()
         res = []
         for s in srcs:
-            depth = torch.empty(v1 - v0, dtype=torch.int32)
-            pred = torch.empty(v1 - v0, dtype=torch.int32)
-            levels = grd.bfs_partitioned(part, ex, s, depth, pred)
-            res.append((depth, pred, levels))
+            for direction in ("push", "pull", "auto"):
+                if direction == "pull" and graph_name == "directed":
+                    continue  # pull reads out-lists as in-lists: symmetric graphs only
+                depth = torch.empty(v1 - v0, dtype=torch.int32)
+                pred = torch.empty(v1 - v0, dtype=torch.int32)
+                levels = grd.bfs_partitioned(part, ex, s, depth, pred, direction=direction)
+                res.append((depth, pred, levels))
         out[rank] = [(d.numpy().copy(), p.numpy().copy(), L) for d, p, L in res]
     finally:
         dist.destroy_process_group()
@@ -133,7 +165,9 @@ def test_partitioned_bfs_world2_gloo(graph_name):
     out = mgr.dict()
     mp.spawn(_worker, args=(2, _free_port(), graph_name, srcs, out), nprocs=2, join=True)
     R, C, _ = g.numpy()
-    for k, s in enumerate(srcs):
+    per_src = 2 if graph_name == "directed" else 3
+    for k in range(len(out[0])):
+        s = srcs[k // per_src]
         depth = np.concatenate([out[r][k][0] for r in range(2)])
         pred = np.concatenate([out[r][k][1] for r in range(2)])
         ref, _ = oracle.bfs(R, C, s)

@@ -30,17 +30,19 @@ def grd():
     return dist
 
 
-def _loopback(grd, g, P, srcs):
+def _loopback(grd, g, P, srcs, directions=("push", "pull", "auto")):
     parts = []
     for r in range(P):
         v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, P, r)
-        parts.append(grd.GpuPartition(Rl.cuda(), Cl.cuda(), g.n, P, r))
+        parts.append(grd.GpuPartition(Rl.cuda(), Cl.cuda(), g.n, P, r, symmetric=g.symmetric))
     grp = grd.LoopbackGroup(parts)
     R, C, _ = g.numpy()
-    for s in srcs:
+    if not g.symmetric:
+        directions = ("push",)
+    for s, direction in [(s, d) for s in srcs for d in directions]:
         depths = [torch.empty(pt.n_local, dtype=torch.int32, device="cuda") for pt in parts]
         preds = [torch.empty(pt.n_local, dtype=torch.int32, device="cuda") for pt in parts]
-        levels = grp.bfs(s, depths, preds)
+        levels = grp.bfs(s, depths, preds, direction=direction)
         depth = torch.cat(depths).cpu().numpy()
         pred = torch.cat(preds).cpu().numpy()
         ref, _ = oracle.bfs(R, C, s)
@@ -89,10 +91,10 @@ def test_world1_nccl_group(grd):
         part = grd.GpuPartition(Rl.cuda(), Cl.cuda(), g.n, 1, 0)
         ex = grd.TorchDistExchange()
         R, C, _ = g.numpy()
-        for s in gg.sources(g, 2):
+        for s, direction in [(s, d) for s in gg.sources(g, 2) for d in ("push", "pull", "auto")]:
             depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
             pred = torch.empty(g.n, dtype=torch.int32, device="cuda")
-            grd.bfs_partitioned(part, ex, s, depth, pred)
+            grd.bfs_partitioned(part, ex, s, depth, pred, direction=direction)
             ref, _ = oracle.bfs(R, C, s)
             assert np.array_equal(depth.cpu().numpy(), ref)
             assert oracle.check_bfs(R, C, s, depth.cpu().numpy(), pred.cpu().numpy()) == []
