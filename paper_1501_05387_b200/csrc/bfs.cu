@@ -252,56 +252,86 @@ __device__ __forceinline__ void pull_level(const BfsArgs &a, const uint32_t *__r
     const int64_t wb1 = nwords * (blockIdx.x + 1) / gridDim.x;
     const unsigned l = lane_id();
     const unsigned long long pol = policy_evict_first();
+    const bool sym = a.Rt == a.R;
+    // kPW words per grab, processed in phases so their loads overlap: row
+    // offsets of all kPW vertices, then their FIRST in-neighbour and its
+    // frontier bit (most candidates resolve there: C2 averages 1.8 inspected
+    // edges per candidate), then the remaining lists of the unresolved ones.
+#ifndef GR_PULL_WORDS
+#define GR_PULL_WORDS 2
+#endif
+    constexpr int kPW = GR_PULL_WORDS;
     for (;;) {
         int c = 0;
-        if (l == 0) c = atomicAdd(swork, 1);
+        if (l == 0) c = atomicAdd(swork, kPW);
         c = __shfl_sync(0xffffffffu, c, 0);
-        const int64_t wi = wb0 + c;
-        if (wi >= wb1) break;
-        const int64_t v = wi * 32 + l;
-        const uint32_t visw = a.visited[wi];
-        if (visw == 0xffffffffu) {  // every vertex of the word already visited
-            if (l == 0) fnext[wi] = 0u;
-            continue;
+        const int64_t w0 = wb0 + c;
+        if (w0 >= wb1) break;
+        uint32_t visw[kPW];
+        int64_t beg[kPW], end[kPW];
+        int32_t parent[kPW];
+        bool found[kPW];
+#pragma unroll
+        for (int k = 0; k < kPW; ++k) visw[k] = (w0 + k < wb1) ? a.visited[w0 + k] : 0xffffffffu;
+#pragma unroll
+        for (int k = 0; k < kPW; ++k) {
+            const int64_t v = (w0 + k) * 32 + l;
+            const bool cand = v < a.n && !((visw[k] >> l) & 1u);
+            beg[k] = cand ? a.Rt[v] : 0;
+            end[k] = cand ? a.Rt[v + 1] : 0;
         }
-        const bool cand = v < a.n && !((visw >> l) & 1u);
-        bool found = false;
-        int32_t parent = -1;
-        if (cand) {
-            const int64_t beg = a.Rt[v], end = a.Rt[v + 1];
-            for (int64_t e = beg; e < end && !found; e += 4) {
+        int32_t u0[kPW];
+#pragma unroll
+        for (int k = 0; k < kPW; ++k) u0[k] = beg[k] < end[k] ? ld_stream(a.Ct + beg[k], pol) : -1;
+#pragma unroll
+        for (int k = 0; k < kPW; ++k) {
+            const uint32_t fw = u0[k] >= 0 ? __ldg(fcur + (u0[k] >> 5)) : 0u;
+            found[k] = u0[k] >= 0 && ((fw >> (u0[k] & 31)) & 1u);
+            parent[k] = u0[k];
+            insp += (u0[k] >= 0);
+        }
+#pragma unroll
+        for (int k = 0; k < kPW; ++k) {
+            if (found[k]) continue;
+            for (int64_t e = beg[k] + 1; e < end[k] && !found[k]; e += 4) {
                 int32_t u[4];
                 uint32_t fw[4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) u[k] = (e + k < end) ? ld_stream(a.Ct + e + k, pol) : -1;
+                for (int q = 0; q < 4; ++q) u[q] = (e + q < end[k]) ? ld_stream(a.Ct + e + q, pol) : -1;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) fw[k] = (u[k] >= 0) ? __ldg(fcur + (u[k] >> 5)) : 0u;
+                for (int q = 0; q < 4; ++q) fw[q] = (u[q] >= 0) ? __ldg(fcur + (u[q] >> 5)) : 0u;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    if (!found && u[k] >= 0) {
+                for (int q = 0; q < 4; ++q) {
+                    if (!found[k] && u[q] >= 0) {
                         ++insp;
-                        if ((fw[k] >> (u[k] & 31)) & 1u) {
-                            found = true;
-                            parent = u[k];
+                        if ((fw[q] >> (u[q] & 31)) & 1u) {
+                            found[k] = true;
+                            parent[k] = u[q];
                         }
                     }
                 }
             }
         }
-        const unsigned nb = __ballot_sync(0xffffffffu, found);
-        if (l == 0) {
-            fnext[wi] = nb;
-            if (nb) a.visited[wi] = visw | nb;
+#pragma unroll
+        for (int k = 0; k < kPW; ++k) {
+            const int64_t wi = w0 + k;
+            if (wi >= wb1) break;
+            const int64_t v = wi * 32 + l;
+            const unsigned nb = __ballot_sync(0xffffffffu, found[k]);
+            if (l == 0) {
+                fnext[wi] = nb;
+                if (nb) a.visited[wi] = visw[k] | nb;
+            }
+            if (nb == 0) continue;
+            int64_t deg = 0;
+            if (found[k]) {
+                a.depth[v] = next_depth;
+                if (a.pred) a.pred[v] = parent[k];
+                deg = sym ? end[k] - beg[k] : a.R[v + 1] - a.R[v];
+            }
+            ndisc += found[k];
+            app.push(found[k] && deg > 0, (int32_t)v, deg);
         }
-        if (nb == 0) continue;
-        int64_t deg = 0;
-        if (found) {
-            a.depth[v] = next_depth;
-            if (a.pred) a.pred[v] = parent;
-            deg = a.R[v + 1] - a.R[v];
-        }
-        ndisc += found;
-        app.push(found && deg > 0, (int32_t)v, deg);
     }
 }
 
