@@ -26,6 +26,9 @@ import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# the image sets NCCL_DEBUG=VERSION, which prints a banner on STDOUT and breaks
+# the one-JSON-line contract; keep NCCL to warnings (on stderr) unless asked
+os.environ["NCCL_DEBUG"] = os.environ.get("GR_NCCL_DEBUG", "WARN")
 sys.path.insert(0, ROOT)
 
 METRIC = "BFS/SSSP GTEPS at 1/2/4/8 B200; achieved HBM GB/s as fraction of roofline"
