@@ -29,6 +29,14 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 # the image sets NCCL_DEBUG=VERSION, which prints a banner on STDOUT and breaks
 # the one-JSON-line contract; keep NCCL to warnings (on stderr) unless asked
 os.environ["NCCL_DEBUG"] = os.environ.get("GR_NCCL_DEBUG", "WARN")
+# Anything native libraries print on fd 1 goes to stderr; the JSON line is
+# written to a saved duplicate of the real stdout.
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(obj):
+    os.write(_JSON_FD, (json.dumps(obj) + "\n").encode())
 sys.path.insert(0, ROOT)
 
 METRIC = "BFS/SSSP GTEPS at 1/2/4/8 B200; achieved HBM GB/s as fraction of roofline"
@@ -198,7 +206,7 @@ def run_reference(args, rank, world):
                             "sample": "%d %s traversals of %s (one per step), single-threaded C oracle"
                                       % (args.steps, args.prim, args.config)},
            "e2e": {"value": value, "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 # ----------------------------------------------------------------- partitioned (multi-GPU) arm
@@ -268,7 +276,7 @@ def run_partitioned(args, rank, world, dev):
                "clocks": clk.summary(),
                "roofline": None,
                "e2e": None}
-        print(json.dumps(out), flush=True)
+        emit(out)
     part.close()
     dist.destroy_process_group()
 
@@ -438,7 +446,7 @@ def main():
                                          "single-threaded C oracle (%d host cores available)"
                                          % (cnt, args.prim, args.config, os.cpu_count())}
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     G.close()
     if world > 1:
         dist.destroy_process_group()
