@@ -25,10 +25,10 @@
 namespace gr {
 
 #ifndef GR_SMALL_CAP
-#define GR_SMALL_CAP 2048
+#define GR_SMALL_CAP 512  // measured: smaller shared memory leaves more L1 for probes/spills
 #endif
 constexpr int64_t kSmallF = GR_SMALL_CAP;  // small mode: queue capacity (shared memory)
-constexpr int64_t kSmallFDefault = 1024;  // small mode: default max frontier (swept on C4)
+constexpr int64_t kSmallFDefault = 512;   // small mode: default max frontier (swept on C4)
 constexpr int64_t kSmallE = 16384;  // small mode: max frontier edges
 #ifndef GR_BFS_STAGES
 #define GR_BFS_STAGES 0  // measured on C2 push: 2 and 4 stages are slower (smem displaces L1)

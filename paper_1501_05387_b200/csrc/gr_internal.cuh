@@ -25,7 +25,7 @@ constexpr int kBlock = GR_BLOCK;         // threads per CTA of the persistent ke
 constexpr int kMinBlocks = GR_MINB;      // resident CTAs per SM the kernels are built for
 constexpr int kWarpsPerBlock = kBlock / kWarp;
 #ifndef GR_STAGE_CAP
-#define GR_STAGE_CAP 256
+#define GR_STAGE_CAP 128
 #endif
 constexpr int kStageCap = GR_STAGE_CAP;  // per-warp smem staging of appended vertices
 constexpr int kMaxStatRecords = 1 << 16; // per-level records kept for gr_get_run_stats
