@@ -1,0 +1,94 @@
+"""ablation of the hot path's variants on B200, the analog of
+the paper's Fig. exp_optimization and its DO speedup claim
+(1.52x scale-free, 1.28x small-degree large-diameter):
+
+  * load balancing: merge-path over edges (lb) vs thread/warp/CTA (twc) vs auto
+  * idempotent discovery on/off
+  * direction: push only vs direction-optimizing (Beamer rule) vs the paper's
+    literal rule "unvisited < frontier" (switch_rule=1)
+
+Times are device times of the whole traversal (CUDA events), mean over the
+sources, L2 warm (no flush: this compares variants, bench.py gives the
+headline numbers). Writes a markdown table to stdout and JSON to --out.
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import graphgen as gg
+import paper_1501_05387_b200 as gr
+
+VARIANTS = [
+    ("push lb", dict(direction="push", strategy="lb")),
+    ("push twc", dict(direction="push", strategy="twc")),
+    ("push auto", dict(direction="push", strategy="auto")),
+    ("push auto idempotent", dict(direction="push", strategy="auto", idempotent=True)),
+    ("DO Beamer", dict(direction="auto", strategy="auto")),
+    ("DO paper-literal", dict(direction="auto", strategy="auto", switch_rule=1)),
+    ("DO Beamer idempotent", dict(direction="auto", strategy="auto", idempotent=True)),
+]
+
+
+def run(cfg, nsrc, reps):
+    torch.cuda.set_device(0)
+    g = gg.make_config(cfg, device="cuda", weights=False)
+    G = gr.Graph(g.R, g.C, None, symmetric=True)
+    deg = g.R[1:] - g.R[:-1]
+    srcs = gg.sources(g, nsrc)
+    rows = []
+    for name, kw in VARIANTS:
+        ms, edges, insp, levels = 0.0, 0, 0, 0
+        for s in srcs:
+            G.bfs(s, **kw)  # warm
+            for _ in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                depth, _ = G.bfs(s, **kw)
+                e1.record()
+                torch.cuda.synchronize()
+                ms += e0.elapsed_time(e1)
+                st = G.run_stats()
+                insp += sum(r["inspected_edges"] for r in st["levels"])
+                levels += st["num_levels"]
+                edges += int(deg[depth >= 0].sum())
+        k = len(srcs) * reps
+        rows.append(dict(variant=name, ms=ms / k, gteps=edges / (ms * 1e-3) / 1e9,
+                         inspected_edges=insp / k, levels=levels / k))
+    G.close()
+    return dict(config=cfg, n=g.n, m=g.m, rows=rows)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="c2_kron21,c3_orkut,c4_road")
+    ap.add_argument("--nsrc", type=int, default=4)
+    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    res = []
+    for cfg in a.configs.split(","):
+        nsrc = 2 if cfg == "c4_road" else a.nsrc
+        reps = 1 if cfg == "c4_road" else a.reps
+        r = run(cfg, nsrc, reps)
+        res.append(r)
+        print("\n### %s (n=%d, m=%d)\n" % (cfg, r["n"], r["m"]))
+        print("| variant | ms / BFS | GTEPS | edges inspected / BFS | levels |")
+        print("|---|---|---|---|---|")
+        for row in r["rows"]:
+            print("| %s | %.3f | %.1f | %.3g | %.1f |" % (row["variant"], row["ms"], row["gteps"],
+                                                         row["inspected_edges"], row["levels"]))
+        by = {row["variant"]: row for row in r["rows"]}
+        print("\nDO speedup over push-only (auto strategy): %.2fx (Beamer), %.2fx (paper-literal)"
+              % (by["push auto"]["ms"] / by["DO Beamer"]["ms"], by["push auto"]["ms"] / by["DO paper-literal"]["ms"]))
+        sys.stdout.flush()
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
