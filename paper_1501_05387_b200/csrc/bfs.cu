@@ -131,7 +131,14 @@ struct BfsPushOp {
             const int32_t w = dst[u];
             const uint32_t bit = 1u << (w & 31);
             disc[u] = false;
-            if (ok[u] && !(word[u] & bit)) {
+            bool cand = ok[u] && !(word[u] & bit);
+            if (idempotent) {
+                // warp-level culling heuristic (A-5 i): lanes of one warp that
+                // target the same vertex keep only the lowest lane
+                const unsigned peers = __match_any_sync(0xffffffffu, cand ? w : -1 - (int)lane_id());
+                cand = cand && (__ffs(peers) - 1 == (int)lane_id());
+            }
+            if (cand) {
                 if (idempotent) {
                     if (*(volatile int32_t *)(depth + w) < 0) {
                         disc[u] = true;
@@ -444,7 +451,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
     app.sd = s->u.stage.sd[wib];
     app.cnt = 0;
     app.S = a.S;
-    app.cap = a.n;
+    app.cap = 2 * a.n;  // queues hold 2n entries (idempotent duplicates)
     app.overflow = &a.ctl->overflow;
 
     for (;;) {

@@ -240,10 +240,11 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
     TRYC(cudaGetLastError());
     for (int i = 0; i < 3; ++i) TRY(dev_alloc(g, (void **)&g->fbuf[i], nw * sizeof(uint32_t)));
     for (int i = 0; i < 2; ++i) {
-        TRY(dev_alloc(g, (void **)&g->qv[i], n * sizeof(int32_t)));
-        TRY(dev_alloc(g, (void **)&g->qo[i], n * sizeof(int64_t)));
+        // 2n: room for the duplicates of idempotent (atomic-free) discovery
+        TRY(dev_alloc(g, (void **)&g->qv[i], 2 * n * sizeof(int32_t)));
+        TRY(dev_alloc(g, (void **)&g->qo[i], 2 * n * sizeof(int64_t)));
     }
-    g->pack_shift = bits_for(n + 1);
+    g->pack_shift = bits_for(2 * n + 1);
     TRY(dev_alloc(g, (void **)&g->ctl, sizeof(Ctl)));
     TRYC(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s));
     TRY(dev_alloc(g, (void **)&g->stats_dev, kMaxStatRecords * sizeof(gr_level_stats)));
