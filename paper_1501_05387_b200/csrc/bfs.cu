@@ -150,6 +150,12 @@ struct BfsPushOp {
                 }
             }
         }
+        // small levels (no probe): the degree of every candidate is loaded in
+        // parallel with its claim, off the critical path of the level
+        int32_t sdeg[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            sdeg[u] = (probe == 0 && ok[u]) ? (int32_t)(R[dst[u] + 1] - R[dst[u]]) : 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (!__any_sync(0xffffffffu, disc[u])) continue;
@@ -159,7 +165,7 @@ struct BfsPushOp {
                 depth[w] = next_depth;
                 if (pred) pred[w] = src[u];
                 if (fbn) atomicOr(fbn + (w >> 5), 1u << (w & 31));  // RED.OR
-                deg = R[w + 1] - R[w];
+                deg = probe == 0 ? (int64_t)sdeg[u] : R[w + 1] - R[w];
                 ++ndisc;
             }
             app->push(disc[u] && deg > 0, w, deg);
@@ -463,6 +469,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
             const unsigned long long q0 = ld_relaxed(&cur.qpack), q1 = ld_relaxed(&cur.ndisc),
                                      q2 = ld_relaxed(&cur.insp), q3 = ld_relaxed(&a.ctl->overflow);
             s->ctl[0] = q0; s->ctl[1] = q1; s->ctl[2] = q2; s->ctl[3] = q3;
+            // per-level CTA counters, reset before the barrier below (racecheck)
+            s->work = 0; s->bsum[0] = 0; s->bsum[1] = 0;
         }
         __syncthreads();
         const unsigned long long qp = s->ctl[0];
@@ -616,7 +624,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                 sr.discovered = 0; sr.inspected_edges = (dir == 1) ? mf : 0; sr.aux = st.u_cnt; sr.ns = 0;
             }
         }
-        if (threadIdx.x == 0) { s->work = 0; s->bsum[0] = 0; s->bsum[1] = 0; }
         Slot &nxt = a.ctl->slot[(L + 1) & 3];
         app.qv = a.qv[(L + 1) & 1];
         app.qo = a.qo[(L + 1) & 1];

@@ -1,0 +1,26 @@
+"""compute-sanitizer over every kernel path on small graphs:
+memcheck (out-of-bounds / misaligned), racecheck (shared-memory hazards),
+synccheck (barrier misuse). scripts/sanitize.py runs BFS in every direction x
+strategy and SSSP on symmetric and directed graphs and checks the oracle."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck"])
+def test_sanitizer_clean(tool):
+    import __graft_entry__
+    __graft_entry__.build()
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    r = subprocess.run([exe, "--tool", tool, "--error-exitcode", "3", sys.executable,
+                        os.path.join(ROOT, "scripts", "sanitize.py")],
+                       capture_output=True, text=True, timeout=900)
+    out = r.stdout + r.stderr
+    assert "sanitize workload ok" in out, out[-3000:]
+    assert r.returncode == 0, out[-3000:]
