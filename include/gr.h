@@ -50,8 +50,12 @@ enum {
                                undirected inputs); pull then
                                reads the CSR as its own CSC. Without it the library
                                builds the reverse graph (CSC) on the device (A-18). */
-    GR_VALIDATE = 1u << 2   /* O(n+m) CSR checks on the device:
+    GR_VALIDATE = 1u << 2,  /* O(n+m) CSR checks on the device:
                                R[0]=0, R non-decreasing, R[n]=m, 0<=C[e]<n.       */
+    GR_KEEP_ORDER = 1u << 3 /* keep the caller's neighbour order. By default every
+                               in-list is reordered by neighbour degree (descending)
+                               so pull steps exit early sooner; results (depth,
+                               dist) are unaffected, the parent picked may differ. */
 };
 
 /*

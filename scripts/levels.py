@@ -15,8 +15,33 @@ ap.add_argument("--maxrows", type=int, default=40)
 a = ap.parse_args()
 torch.cuda.set_device(0)
 g = gg.make_config(a.config, device="cuda", weights=(a.prim == "sssp") or None)
+SRCS = gg.sources(g, a.nsrc)
+if os.environ.get("NBRSORT"):  # experiment: each list ordered by neighbour degree, descending
+    deg = g.R[1:] - g.R[:-1]
+    src_e = torch.repeat_interleave(torch.arange(g.n, device="cuda"), deg)
+    key = src_e * (int(deg.max()) + 1) + (int(deg.max()) - deg[g.C.long()])
+    order = torch.argsort(key, stable=True)
+    g = gg.Graph(g.n, g.R, g.C[order].contiguous(), None if g.W is None else g.W[order].contiguous(), True, g.meta)
+    print("neighbour lists sorted by degree")
+if os.environ.get("RELABEL"):  # experiment: degree-descending vertex order
+    deg = g.R[1:] - g.R[:-1]
+    new2old = torch.argsort(-deg * g.n - torch.arange(g.n, device="cuda"), stable=True)
+    new2old = torch.sort(-deg, stable=True).indices
+    old2new = torch.empty_like(new2old)
+    old2new[new2old] = torch.arange(g.n, device="cuda")
+    src_e = torch.repeat_interleave(torch.arange(g.n, device="cuda"), deg)
+    key = old2new[src_e] * g.n + old2new[g.C.long()]
+    order = torch.argsort(key)
+    key = key[order]
+    C2 = (key % g.n).to(torch.int32)
+    R2 = torch.zeros(g.n + 1, dtype=torch.int64, device="cuda")
+    R2[1:] = torch.cumsum(deg[new2old], 0)
+    W2 = None if g.W is None else g.W[order]
+    g = gg.Graph(g.n, R2, C2, W2, True, g.meta)
+    SRCS = [int(old2new[s]) for s in SRCS]
+    print("relabelled by degree")
 G = gr.Graph(g.R, g.C, g.W, symmetric=True)
-for s in gg.sources(g, a.nsrc):
+for s in SRCS:
     for d in a.directions.split(","):
         for rep in range(3):
             if a.prim == "bfs":
