@@ -48,6 +48,7 @@ struct BfsArgs {
     uint32_t *fbuf[3];     // rotating frontier bitmaps
     int32_t *qv[2];
     int64_t *qo[2];
+    int64_t *qr[2];
     int32_t *depth;
     int32_t *pred;       // may be null
     Ctl *ctl;
@@ -70,6 +71,7 @@ struct BfsSmem {
             PipeWarpSmem<(kBfsStages > 0 ? kBfsStages : 1), false> pipe[kBfsStages > 0 ? kWarpsPerBlock : 1];
             int32_t sv[kWarpsPerBlock][kStageCap];
             int32_t sd[kWarpsPerBlock][kStageCap];
+            int64_t sr[kWarpsPerBlock][kStageCap];
         } stage;
         struct {  // small mode: the frontier lives here (double-buffered)
             int64_t rs[2][kSmallF];   // row start of each entry
@@ -150,25 +152,20 @@ struct BfsPushOp {
                 }
             }
         }
-        // small levels (no probe): the degree of every candidate is loaded in
-        // parallel with its claim, off the critical path of the level
-        int32_t sdeg[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            sdeg[u] = (probe == 0 && ok[u]) ? (int32_t)(R[dst[u] + 1] - R[dst[u]]) : 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (!__any_sync(0xffffffffu, disc[u])) continue;
             const int32_t w = dst[u];
-            int64_t deg = 0;
+            int64_t deg = 0, rs = 0;
             if (disc[u]) {
                 depth[w] = next_depth;
                 if (pred) pred[w] = src[u];
                 if (fbn) atomicOr(fbn + (w >> 5), 1u << (w & 31));  // RED.OR
-                deg = probe == 0 ? (int64_t)sdeg[u] : R[w + 1] - R[w];
+                rs = R[w];
+                deg = R[w + 1] - rs;
                 ++ndisc;
             }
-            app->push(disc[u] && deg > 0, w, deg);
+            app->push(disc[u] && deg > 0, w, deg, rs);
         }
     }
 };
@@ -192,6 +189,7 @@ struct SmallPushOp {
     unsigned long long *spk;     // smem packed counter (edges << kSmallCntBits) | count
     int32_t *gq_next;            // global spill queue (entries >= kSmallF)
     int64_t *go_next;
+    int64_t *gr_next;
     unsigned long long ndisc;
 
     __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
@@ -234,6 +232,7 @@ struct SmallPushOp {
                 } else {
                     gq_next[pos] = w;
                     go_next[pos] = off;
+                    gr_next[pos] = rs[u];
                 }
                 if (deg > 0) {
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs[u]));
@@ -336,14 +335,15 @@ __device__ __forceinline__ void pull_level(const BfsArgs &a, const uint32_t *__r
                 if (nb) a.visited[wi] = visw[k] | nb;
             }
             if (nb == 0) continue;
-            int64_t deg = 0;
+            int64_t deg = 0, rs = 0;
             if (found[k]) {
                 a.depth[v] = next_depth;
                 if (a.pred) a.pred[v] = parent[k];
-                deg = sym ? end[k] - beg[k] : a.R[v + 1] - a.R[v];
+                rs = sym ? beg[k] : a.R[v];
+                deg = sym ? end[k] - beg[k] : a.R[v + 1] - rs;
             }
             ndisc += found[k];
-            app.push(found[k] && deg > 0, (int32_t)v, deg);
+            app.push(found[k] && deg > 0, (int32_t)v, deg, rs);
         }
     }
 }
@@ -430,6 +430,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         a.visited[a.src >> 5] |= 1u << (a.src & 31);
         a.qv[0][0] = a.src;
         a.qo[0][0] = 0;
+        a.qr[0][0] = a.R[a.src];
         a.ctl->slot[0].qpack = (deg_src > 0) ? (((unsigned long long)deg_src << a.S) | 1ull) : 0ull;
     }
     grid.sync();
@@ -455,6 +456,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
     Appender app;
     app.sv = s->u.stage.sv[wib];
     app.sd = s->u.stage.sd[wib];
+    app.sr = s->u.stage.sr[wib];
     app.cnt = 0;
     app.S = a.S;
     app.cap = 2 * a.n;  // queues hold 2n entries (idempotent duplicates)
@@ -502,7 +504,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                     const int32_t v = a.qv[L & 1][j];
                     s->u.small.q[0][j] = v;
                     s->u.small.off[0][j] = a.qo[L & 1][j];
-                    s->u.small.rs[0][j] = a.R[v];
+                    s->u.small.rs[0][j] = a.qr[L & 1][j];
                 }
                 if (threadIdx.x < 3) { s->pk[threadIdx.x] = 0; s->nd[threadIdx.x] = 0; }
                 __syncthreads();
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                     }
                     SmallPushOp op{a.visited, a.depth, a.pred, a.R, a.C, Lc + 1, s->u.small.q[c ^ 1],
                                    s->u.small.rs[c ^ 1], s->u.small.off[c ^ 1], &s->pk[r1],
-                                   a.qv[(Lc + 1) & 1], a.qo[(Lc + 1) & 1], 0ull};
+                                   a.qv[(Lc + 1) & 1], a.qo[(Lc + 1) & 1], a.qr[(Lc + 1) & 1], 0ull};
                     SmemFrontier fr{s->u.small.q[c], s->u.small.off[c], s->u.small.rs[c], cf, E};
                     GR_TSTAMP(9);
                     expand_lb(fr, a.C, (int64_t)wib, (int64_t)kWarpsPerBlock, op);
@@ -568,6 +570,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                     for (int64_t j = threadIdx.x; j < cf && j < kSmallF; j += kBlock) {
                         a.qv[st.L & 1][j] = s->u.small.q[c][j];
                         a.qo[st.L & 1][j] = s->u.small.off[c][j];
+                        a.qr[st.L & 1][j] = s->u.small.rs[c][j];
                     }
                     if (mu_pending) st.m_u -= E;
                     if (threadIdx.x == 0) {
@@ -627,6 +630,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         Slot &nxt = a.ctl->slot[(L + 1) & 3];
         app.qv = a.qv[(L + 1) & 1];
         app.qo = a.qo[(L + 1) & 1];
+        app.qr = a.qr[(L + 1) & 1];
         app.counter = &nxt.qpack;
         uint32_t *fb_c = a.fbuf[L % 3];
         uint32_t *fb_n = a.fbuf[(L + 1) % 3];
@@ -654,7 +658,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
             BfsPushOp op{a.visited, st.fbn_clean ? fb_n : nullptr, a.depth, a.pred, a.R, L + 1,
                          a.idempotent, &app, 0ull, pol_keep,
                          mf < (1 << 16) ? 0 : (st.m_u * 4 < a.m ? 2 : 1)};
-            GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.R, f, mf};
+            GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.qr[L & 1], f, mf};
             // auto (reading A-4, measured on B200): node-granular thread/warp/CTA
             // when the frontier's lists are short on average (mesh-like levels:
             // no frontier-wide search, 35% faster per level on C4); merge-path
@@ -711,7 +715,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.visited = g->visited;
     a.noin = g->noin;
     for (int i = 0; i < 3; ++i) a.fbuf[i] = g->fbuf[i];
-    for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; }
+    for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.qr[i] = g->qr[i]; }
     a.depth = depth; a.pred = pred;
     a.ctl = g->ctl; a.stats = g->stats_dev;
     a.src = src;

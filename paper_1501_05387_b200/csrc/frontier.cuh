@@ -55,9 +55,12 @@ template <int kCap>
 struct AppenderT {
     int32_t *sv;                    // smem staging [kCap]
     int32_t *sd;                    // smem staging degrees [kCap] (offsets mode)
+    int64_t *sr;                    // smem staging row starts [kCap] (offsets mode)
     int cnt;                        // warp-uniform
     int32_t *qv;                    // destination queue
     int64_t *qo;                    // destination prefix (null: count-only queue)
+    int64_t *qr;                    // destination row starts R[v] (offsets mode): the
+                                    // next level reads its lists without touching R
     unsigned long long *counter;    // packed (edges << S) | count, or plain count
     int S;                          // count-field bits (offsets mode)
     int64_t cap;                    // queue capacity
@@ -94,7 +97,10 @@ struct AppenderT {
                 const int j = r * 32 + (int)l;
                 if (j < k) {
                     qv[cbase + j] = sv[j];
-                    if (qo) qo[cbase + j] = ebase + incl[r];
+                    if (qo) {
+                        qo[cbase + j] = ebase + incl[r];
+                        qr[cbase + j] = sr[j];
+                    }
                 }
             }
         }
@@ -102,11 +108,12 @@ struct AppenderT {
         cnt = 0;
     }
 
-    __device__ __forceinline__ void push(bool has, int32_t v, int64_t d) {
+    // v: vertex, d: its out-degree, rs: R[v] (offsets mode)
+    __device__ __forceinline__ void push(bool has, int32_t v, int64_t d, int64_t rs = 0) {
         const unsigned mask = __ballot_sync(0xffffffffu, has);
         if (mask == 0) return;
         const int pos = cnt + __popc(mask & lanemask_lt());
-        if (has) { sv[pos] = v; if (qo) sd[pos] = (int32_t)d; }
+        if (has) { sv[pos] = v; if (qo) { sd[pos] = (int32_t)d; sr[pos] = rs; } }
         cnt += __popc(mask);
         __syncwarp();
         if (cnt > kCap - 32) flush();
@@ -186,22 +193,25 @@ __device__ __forceinline__ int64_t warp_lower_bound(int64_t F, int64_t t, Key ke
 
 // ---------------------------------------------------------------------------
 // Frontier views: where the queue of the current level lives.
-//   GlobalFrontier: vertex ids + exclusive degree prefix in global memory,
-//                   row starts read from R (grid-wide levels).
-//   SmemFrontier:   the same three arrays in shared memory (single-CTA levels;
-//                   the row start was cached when the prefix was built).
+//   GlobalFrontier: vertex ids, exclusive degree prefix and row starts R[v]
+//                   in global memory (grid-wide levels). The filter wrote all
+//                   three when it appended the vertex, so loading an entry is
+//                   three independent coalesced loads (no dependent R[v]
+//                   lookup: one memory round trip less per level). Entries are
+//                   contiguous in edge space, so deg(j) = qo[j+1] - qo[j].
+//   SmemFrontier:   the same three arrays in shared memory (single-CTA levels).
 // ---------------------------------------------------------------------------
 struct GlobalFrontier {
     const int32_t *qv;
     const int64_t *qo;
-    const int64_t *R;
+    const int64_t *qr;
     int64_t F, E;
     __device__ __forceinline__ int64_t off(int64_t i) const { return __ldcg(qo + i); }
     __device__ __forceinline__ void load(int64_t j, int32_t &v, int64_t &o, int64_t &rs, int64_t &end) const {
         v = __ldcg(qv + j);
         o = __ldcg(qo + j);
-        rs = R[v];
-        end = o + (R[v + 1] - rs);
+        rs = __ldcg(qr + j);
+        end = (j + 1 < F) ? __ldcg(qo + j + 1) : E;
     }
 };
 

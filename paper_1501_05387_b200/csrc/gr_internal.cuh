@@ -25,7 +25,7 @@ constexpr int kBlock = GR_BLOCK;         // threads per CTA of the persistent ke
 constexpr int kMinBlocks = GR_MINB;      // resident CTAs per SM the kernels are built for
 constexpr int kWarpsPerBlock = kBlock / kWarp;
 #ifndef GR_STAGE_CAP
-#define GR_STAGE_CAP 128
+#define GR_STAGE_CAP 64    // 64 measured better than 128 (smaller smem leaves more L1)
 #endif
 constexpr int kStageCap = GR_STAGE_CAP;  // per-warp smem staging of appended vertices
 constexpr int kMaxStatRecords = 1 << 16; // per-level records kept for gr_get_run_stats
@@ -91,6 +91,7 @@ struct Graph {
     uint32_t *fbuf[3] = {nullptr, nullptr, nullptr}; // rotating frontier bitmaps
     int32_t *qv[2] = {nullptr, nullptr};    // frontier queues (vertex ids)
     int64_t *qo[2] = {nullptr, nullptr};    // exclusive prefix of degrees
+    int64_t *qr[2] = {nullptr, nullptr};    // row start R[v] of each queue entry
     int32_t *depth_buf = nullptr; // internal outputs when caller passes host memory
     int32_t *pred_buf = nullptr;
     uint32_t *dist_buf = nullptr;

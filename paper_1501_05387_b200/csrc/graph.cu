@@ -24,7 +24,7 @@ gr_status dev_alloc(Graph *g, void **p, size_t bytes) {
 void dev_free_all(Graph *g) {
     void *ptrs[] = {g->R, g->C, g->W, (g->Rt != g->R) ? g->Rt : nullptr,
                     (g->Ct != g->C) ? g->Ct : nullptr, g->visited, g->noin, g->fbuf[0], g->fbuf[1], g->fbuf[2],
-                    g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->depth_buf, g->pred_buf,
+                    g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->qr[0], g->qr[1], g->depth_buf, g->pred_buf,
                     g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev,
                     g->sent, g->send_pairs, g->send_counts, g->recv_pairs};
     for (void *p : ptrs)
@@ -314,6 +314,7 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
         // 2n: room for the duplicates of idempotent (atomic-free) discovery
         TRY(dev_alloc(g, (void **)&g->qv[i], 2 * n * sizeof(int32_t)));
         TRY(dev_alloc(g, (void **)&g->qo[i], 2 * n * sizeof(int64_t)));
+        TRY(dev_alloc(g, (void **)&g->qr[i], 2 * n * sizeof(int64_t)));
     }
     g->pack_shift = bits_for(2 * n + 1);
     TRY(dev_alloc(g, (void **)&g->ctl, sizeof(Ctl)));

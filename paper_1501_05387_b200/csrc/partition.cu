@@ -33,6 +33,7 @@ struct PartArgs {
     int32_t *depth, *pred;
     int32_t *qv[2];
     int64_t *qo[2];
+    int64_t *qr[2];
     Ctl *ctl;
     int S;
 };
@@ -61,6 +62,7 @@ __global__ void part_seed_kernel(PartArgs a, int64_t src) {
     const int64_t d = a.R[s + 1] - a.R[s];
     a.qv[0][0] = (int32_t)s;
     a.qo[0][0] = 0;
+    a.qr[0][0] = a.R[s];
     a.ctl->slot[0].qpack = d > 0 ? (((unsigned long long)d << a.S) | 1ull) : 0ull;
 }
 
@@ -91,13 +93,14 @@ struct PartPushOp {
                     ship = !(atomicOr(a->sent + (w >> 5), bit) & bit);
             }
             const int32_t parent = (int32_t)(a->v_begin + src[u]);
-            int64_t deg = 0;
+            int64_t deg = 0, rs = 0;
             if (disc) {
                 a->depth[lw] = next_depth;
                 if (a->pred) a->pred[lw] = parent;
-                deg = a->R[lw + 1] - a->R[lw];
+                rs = a->R[lw];
+                deg = a->R[lw + 1] - rs;
             }
-            app->push(disc && deg > 0, (int32_t)lw, deg);
+            app->push(disc && deg > 0, (int32_t)lw, deg, rs);
             // remote: bucket (w, parent) for owner q, one atomic per owner per warp
             const unsigned shipm = __ballot_sync(0xffffffffu, ship);
             if (shipm) {
@@ -123,6 +126,7 @@ struct PartPushOp {
 __global__ void __launch_bounds__(kPartBlock) part_expand_kernel(PartArgs a, int level) {
     __shared__ int32_t s_v[kPartWarps][kPartStage];
     __shared__ int32_t s_d[kPartWarps][kPartStage];
+    __shared__ int64_t s_r[kPartWarps][kPartStage];
     const int wib = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -134,13 +138,15 @@ __global__ void __launch_bounds__(kPartBlock) part_expand_kernel(PartArgs a, int
         r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull;
     }
     PartAppender app;
-    app.sv = s_v[wib]; app.sd = s_d[wib]; app.cnt = 0; app.S = a.S; app.cap = a.n_local;
+    app.sv = s_v[wib]; app.sd = s_d[wib]; app.sr = s_r[wib]; app.cnt = 0; app.S = a.S;
+    app.cap = 2 * a.n_local;
     app.overflow = &a.ctl->overflow;
     app.qv = a.qv[(level + 1) & 1];
     app.qo = a.qo[(level + 1) & 1];
+    app.qr = a.qr[(level + 1) & 1];
     app.counter = &a.ctl->slot[(level + 1) & 3].qpack;
     PartPushOp op{&a, level + 1, &app};
-    GlobalFrontier fr{a.qv[level & 1], a.qo[level & 1], a.R, f, mf};
+    GlobalFrontier fr{a.qv[level & 1], a.qo[level & 1], a.qr[level & 1], f, mf};
     expand_lb(fr, a.C, gw, nw, op);
     app.finish();
 }
@@ -149,19 +155,22 @@ __global__ void __launch_bounds__(kPartBlock) part_absorb_kernel(PartArgs a, int
                                                                  int64_t nrecv) {
     __shared__ int32_t s_v[kPartWarps][kPartStage];
     __shared__ int32_t s_d[kPartWarps][kPartStage];
+    __shared__ int64_t s_r[kPartWarps][kPartStage];
     const int wib = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     PartAppender app;
-    app.sv = s_v[wib]; app.sd = s_d[wib]; app.cnt = 0; app.S = a.S; app.cap = a.n_local;
+    app.sv = s_v[wib]; app.sd = s_d[wib]; app.sr = s_r[wib]; app.cnt = 0; app.S = a.S;
+    app.cap = 2 * a.n_local;
     app.overflow = &a.ctl->overflow;
     app.qv = a.qv[(level + 1) & 1];
     app.qo = a.qo[(level + 1) & 1];
+    app.qr = a.qr[(level + 1) & 1];
     app.counter = &a.ctl->slot[(level + 1) & 3].qpack;
     for (int64_t base = gw * 32; base < nrecv; base += nw * 32) {
         const int64_t j = base + lane_id();
         bool disc = false;
-        int64_t lw = 0, deg = 0;
+        int64_t lw = 0, deg = 0, rs = 0;
         if (j < nrecv) {
             const int32_t w = pairs[2 * j], parent = pairs[2 * j + 1];
             lw = (int64_t)w - a.v_begin;
@@ -173,11 +182,12 @@ __global__ void __launch_bounds__(kPartBlock) part_absorb_kernel(PartArgs a, int
                 if (disc) {
                     a.depth[lw] = level + 1;
                     if (a.pred) a.pred[lw] = parent;
-                    deg = a.R[lw + 1] - a.R[lw];
+                    rs = a.R[lw];
+                    deg = a.R[lw + 1] - rs;
                 }
             }
         }
-        app.push(disc && deg > 0, (int32_t)lw, deg);
+        app.push(disc && deg > 0, (int32_t)lw, deg, rs);
     }
     app.finish();
 }
@@ -207,6 +217,7 @@ __global__ void part_shard_fill_kernel(PartArgs a, int level, uint32_t *shard) {
 __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int level, const uint32_t *gfront) {
     __shared__ int32_t s_v[kPartWarps][kPartStage];
     __shared__ int32_t s_d[kPartWarps][kPartStage];
+    __shared__ int64_t s_r[kPartWarps][kPartStage];
     const int wib = threadIdx.x >> 5;
     const unsigned l = lane_id();
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -216,10 +227,12 @@ __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int l
         r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull;
     }
     PartAppender app;
-    app.sv = s_v[wib]; app.sd = s_d[wib]; app.cnt = 0; app.S = a.S; app.cap = a.n_local;
+    app.sv = s_v[wib]; app.sd = s_d[wib]; app.sr = s_r[wib]; app.cnt = 0; app.S = a.S;
+    app.cap = 2 * a.n_local;
     app.overflow = &a.ctl->overflow;
     app.qv = a.qv[(level + 1) & 1];
     app.qo = a.qo[(level + 1) & 1];
+    app.qr = a.qr[(level + 1) & 1];
     app.counter = &a.ctl->slot[(level + 1) & 3].qpack;
     const unsigned long long pol = policy_evict_first();
     const int64_t nwords = (a.n_local + 31) / 32;
@@ -249,7 +262,7 @@ __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int l
             if (a.pred) a.pred[v] = parent;
             deg = end - beg;
         }
-        app.push(found && deg > 0, (int32_t)v, deg);
+        app.push(found && deg > 0, (int32_t)v, deg, beg);
     }
     app.finish();
 }
@@ -260,7 +273,7 @@ static PartArgs part_args(Graph *g) {
     a.R = g->R; a.C = g->C; a.visited = g->visited; a.sent = g->sent;
     a.send_pairs = g->send_pairs; a.send_counts = g->send_counts;
     a.depth = g->part_depth; a.pred = g->part_pred;
-    for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; }
+    for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.qr[i] = g->qr[i]; }
     a.ctl = g->ctl;
     a.S = g->pack_shift;
     return a;

@@ -23,6 +23,7 @@ struct SsspArgs {
     int32_t *stamp;
     int32_t *qv[2];
     int64_t *qo[2];
+    int64_t *qr[2];
     int32_t *far[2];
     int64_t far_cap;
     Ctl *ctl;
@@ -33,13 +34,22 @@ struct SsspArgs {
 };
 
 constexpr int kSsspStages = 2;     // cp.async pipeline depth (C + W + payload per stage)
-constexpr int kSsspStage = 128;    // append staging per warp (near and far)
+#ifndef GR_SSSP_PIPE
+#define GR_SSSP_PIPE 0  // cp.async pipeline off: its shared memory displaces L1 (measured slower)
+#endif
+#ifndef GR_SSSP_STAGE
+#define GR_SSSP_STAGE 64
+#endif
+constexpr int kSsspStage = GR_SSSP_STAGE;  // append staging per warp (near and far)
 using SsspAppender = AppenderT<kSsspStage>;
 
 struct SsspSmem {
+#if GR_SSSP_PIPE
     PipeWarpSmem<kSsspStages, true> pipe[kWarpsPerBlock];
+#endif
     int32_t sv[kWarpsPerBlock][kSsspStage];   // near staging
     int32_t sd[kWarpsPerBlock][kSsspStage];
+    int64_t sr[kWarpsPerBlock][kSsspStage];
     int32_t fv[kWarpsPerBlock][kSsspStage];   // far staging
     unsigned long long ctl[8];
     unsigned long long bsum[4];
@@ -79,7 +89,7 @@ struct RelaxOp {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             bool to_near = false, to_far = false;
-            int64_t deg = 0;
+            int64_t deg = 0, rs = 0;
             const int32_t v = dst[u];
             const unsigned long long nd = du[u] + w[u];
             if (ok[u] && nd < (cur[u] >> 32)) {
@@ -90,12 +100,12 @@ struct RelaxOp {
                     const int32_t key = key_near + (far ? 1 : 0);
                     if (atomicExch(stamp + v, key) != key) {
                         if (far) to_far = true;
-                        else { to_near = true; deg = R[v + 1] - R[v]; }
+                        else { to_near = true; rs = R[v]; deg = R[v + 1] - rs; }
                     }
                     ++nimp;
                 }
             }
-            nearq->push(to_near && deg > 0, v, deg);
+            nearq->push(to_near && deg > 0, v, deg, rs);
             farq->push(to_far, v, 0);
         }
     }
@@ -138,13 +148,15 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         if (d > 0) {
             a.qv[0][0] = a.src;
             a.qo[0][0] = 0;
+            a.qr[0][0] = a.R[a.src];
             a.ctl->slot[0].qpack = ((unsigned long long)d << a.S) | 1ull;
         }
     }
     grid.sync();
 
     SsspAppender nearq, farq;
-    nearq.sv = s->sv[wib]; nearq.sd = s->sd[wib]; nearq.cnt = 0; nearq.S = a.S; nearq.cap = a.n;
+    nearq.sv = s->sv[wib]; nearq.sd = s->sd[wib]; nearq.sr = s->sr[wib]; nearq.cnt = 0; nearq.S = a.S;
+    nearq.cap = a.n;
     nearq.overflow = &a.ctl->overflow;
     farq.sv = s->fv[wib]; farq.sd = nullptr; farq.cnt = 0; farq.qo = nullptr; farq.S = 0;
     farq.cap = a.far_cap; farq.overflow = &a.ctl->overflow;
@@ -193,6 +205,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         }
         nearq.qv = a.qv[(k + 1) & 1];
         nearq.qo = a.qo[(k + 1) & 1];
+        nearq.qr = a.qr[(k + 1) & 1];
         nearq.counter = &nxt.qpack;
 
         if (f > 0) {
@@ -201,12 +214,16 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             farq.qv = a.far[fp];
             farq.counter = &a.ctl->far_count[fp];
             RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep};
-            GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.R, f, mf};
+            GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.qr[k & 1], f, mf};
             // same auto rule as BFS (reading A-4): short lists -> thread/warp/CTA
             if (mf <= 16 * f)
                 expand_twc(fr, a.C, op, &s->win);
             else
+#if GR_SSSP_PIPE
                 expand_pipe<kSsspStages, true>(fr, a.C, a.W, gw, nw, op, &s->pipe[wib]);
+#else
+                expand_lb(fr, a.C, gw, nw, op);
+#endif
             nearq.finish();
             farq.finish();
             const unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
@@ -253,7 +270,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
                 const int64_t j = base + lane_id();
                 bool to_near = false, to_far = false;
                 int32_t v = 0;
-                int64_t deg = 0;
+                int64_t deg = 0, rs = 0;
                 if (j < fc) {
                     v = far_c[j];
                     const unsigned long long d = ld_probe(a.dp + v, pol_keep) >> 32;
@@ -261,12 +278,12 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
                         const bool nearb = d < thr;
                         const int32_t key = 2 * it + (nearb ? 0 : 1);
                         if (atomicExch(a.stamp + v, key) != key) {
-                            if (nearb) { to_near = true; deg = a.R[v + 1] - a.R[v]; }
+                            if (nearb) { to_near = true; rs = a.R[v]; deg = a.R[v + 1] - rs; }
                             else to_far = true;
                         }
                     }
                 }
-                nearq.push(to_near && deg > 0, v, deg);
+                nearq.push(to_near && deg > 0, v, deg, rs);
                 farq.push(to_far, v, 0);
             }
             nearq.finish();
@@ -293,7 +310,9 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.n = g->n; a.m = g->m;
     a.R = g->R; a.C = g->C; a.W = g->W;
     a.dp = g->dp; a.stamp = g->stamp;
-    for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.far[i] = g->farq[i]; }
+    for (int i = 0; i < 2; ++i) {
+        a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.qr[i] = g->qr[i]; a.far[i] = g->farq[i];
+    }
     a.far_cap = g->far_cap;
     a.ctl = g->ctl; a.stats = g->stats_dev;
     a.src = src;
