@@ -159,6 +159,27 @@ typedef struct {
 gr_status gr_sssp(gr_graph *g, int32_t src, uint32_t *dist_out, int32_t *pred_out,
                   const gr_sssp_opts *opts);
 
+/*
+ * Asynchronous variants: the same traversal (same arguments, same results,
+ * same errors for bad arguments) is only ENQUEUED on g's stream; the call
+ * returns without waiting, so back-to-back runs and the caller's own stream
+ * work (events, copies) run on the device without host round trips between
+ * them (SURVEY §8(d) timing: the CUDA-event time of the call's GPU work).
+ *   depth_out / dist_out / pred_out must be DEVICE memory (else
+ *   GR_ERR_INVALID_ARGUMENT); they are valid once the stream reaches the end
+ *   of the run (gr_graph_sync, or any later stream-ordered consumer).
+ * gr_graph_sync waits for every run enqueued on g, makes the per-level stats
+ * of the last one available (gr_get_run_stats) and reports a queue overflow
+ * of any of them: if exactly one idempotent BFS was pending it is re-run with
+ * exactly-once claims (as gr_bfs does), otherwise GR_ERR_OVERFLOW. gr_bfs /
+ * gr_sssp call gr_graph_sync first when runs are pending.
+ */
+gr_status gr_bfs_async(gr_graph *g, int32_t src, int32_t *depth_out, int32_t *pred_out,
+                       const gr_bfs_opts *opts);
+gr_status gr_sssp_async(gr_graph *g, int32_t src, uint32_t *dist_out, int32_t *pred_out,
+                        const gr_sssp_opts *opts);
+gr_status gr_graph_sync(gr_graph *g);
+
 /* Per-level records of the last gr_bfs / gr_sssp on g (SURVEY §5 tracing). */
 typedef struct {
     int32_t level;           /* BFS level or SSSP iteration                        */

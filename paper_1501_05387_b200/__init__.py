@@ -68,7 +68,8 @@ class gr_run_stats(ctypes.Structure):
 
 _lib = None
 EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
-           "gr_bfs", "gr_sssp", "gr_get_run_stats", "gr_last_error", "gr_kernel_launch_count",
+           "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
+           "gr_get_run_stats", "gr_last_error", "gr_kernel_launch_count",
            "gr_version", "gr_graph_create_part", "gr_part_buffers", "gr_part_bfs_begin",
            "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_shard",
            "gr_part_bfs_pull"]
@@ -94,6 +95,9 @@ def load(path: str = LIB_PATH):
     lib.gr_graph_info_get.argtypes = [p, P(gr_graph_info)]
     lib.gr_bfs.argtypes = [p, ctypes.c_int32, p, p, P(gr_bfs_opts)]
     lib.gr_sssp.argtypes = [p, ctypes.c_int32, p, p, P(gr_sssp_opts)]
+    lib.gr_bfs_async.argtypes = [p, ctypes.c_int32, p, p, P(gr_bfs_opts)]
+    lib.gr_sssp_async.argtypes = [p, ctypes.c_int32, p, p, P(gr_sssp_opts)]
+    lib.gr_graph_sync.argtypes = [p]
     lib.gr_get_run_stats.argtypes = [p, P(gr_run_stats)]
     lib.gr_last_error.restype = ctypes.c_char_p
     lib.gr_kernel_launch_count.restype = ctypes.c_uint64
@@ -109,7 +113,8 @@ def load(path: str = LIB_PATH):
     lib.gr_part_bfs_shard.argtypes = [p, i32, p]
     lib.gr_part_bfs_pull.argtypes = [p, i32, p]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
-              "gr_bfs", "gr_sssp", "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
+              "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
+              "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
               "gr_part_bfs_begin", "gr_part_bfs_expand", "gr_part_bfs_absorb",
               "gr_part_bfs_frontier", "gr_part_bfs_shard", "gr_part_bfs_pull"):
         getattr(lib, f).restype = ctypes.c_int
@@ -143,6 +148,20 @@ def gr_bfs(h, src, depth_ptr, pred_ptr, opts: Optional[gr_bfs_opts] = None):
 def gr_sssp(h, src, dist_ptr, pred_ptr, opts: Optional[gr_sssp_opts] = None):
     _check(load().gr_sssp(h, int(src), dist_ptr, pred_ptr,
                           ctypes.byref(opts) if opts is not None else None))
+
+
+def gr_bfs_async(h, src, depth_ptr, pred_ptr, opts: Optional[gr_bfs_opts] = None):
+    _check(load().gr_bfs_async(h, int(src), depth_ptr, pred_ptr,
+                               ctypes.byref(opts) if opts is not None else None))
+
+
+def gr_sssp_async(h, src, dist_ptr, pred_ptr, opts: Optional[gr_sssp_opts] = None):
+    _check(load().gr_sssp_async(h, int(src), dist_ptr, pred_ptr,
+                                ctypes.byref(opts) if opts is not None else None))
+
+
+def gr_graph_sync(h):
+    _check(load().gr_graph_sync(h))
 
 
 def gr_get_run_stats(h):
@@ -225,7 +244,9 @@ class Graph:
 
     def bfs(self, src: int, depth=None, pred=None, *, want_pred: bool = True,
             direction="auto", strategy="auto", idempotent: bool = False,
-            switch_rule: int = 0, alpha: float = 0.0, beta: float = 0.0, lb_threshold: int = 0):
+            switch_rule: int = 0, alpha: float = 0.0, beta: float = 0.0, lb_threshold: int = 0,
+            asynchronous: bool = False):
+        """BFS from src. asynchronous=True enqueues only (device outputs; see sync())."""
         import torch
         dev = torch.device("cuda", self.device)
         if depth is None:
@@ -237,11 +258,11 @@ class Graph:
                         int(lb_threshold))
         dp, _ = _ptr(depth)
         pp, _ = _ptr(pred)
-        gr_bfs(self.handle, src, dp, pp, o)
+        (gr_bfs_async if asynchronous else gr_bfs)(self.handle, src, dp, pp, o)
         return depth, pred
 
     def sssp(self, src: int, dist=None, pred=None, *, want_pred: bool = True,
-             delta: int = 0, strategy="auto"):
+             delta: int = 0, strategy="auto", asynchronous: bool = False):
         import torch
         dev = torch.device("cuda", self.device)
         if dist is None:
@@ -251,8 +272,12 @@ class Graph:
         o = gr_sssp_opts(int(delta) & 0xFFFFFFFF, STRATEGY.get(strategy, strategy))
         dp, _ = _ptr(dist)
         pp, _ = _ptr(pred)
-        gr_sssp(self.handle, src, dp, pp, o)
+        (gr_sssp_async if asynchronous else gr_sssp)(self.handle, src, dp, pp, o)
         return dist, pred
+
+    def sync(self):
+        """Wait for the asynchronous runs of this graph; raises on a queue overflow."""
+        gr_graph_sync(self.handle)
 
     def run_stats(self):
         st = gr_get_run_stats(self.handle)

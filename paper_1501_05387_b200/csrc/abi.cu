@@ -48,6 +48,7 @@ static gr_status finish_run(Graph *g) {
     unsigned long long levels = 0, overflow = 0;
     GR_CUDA(cudaMemcpyAsync(&levels, &g->ctl->levels, sizeof(levels), cudaMemcpyDeviceToHost, g->stream));
     GR_CUDA(cudaMemcpyAsync(&overflow, &g->ctl->overflow, sizeof(overflow), cudaMemcpyDeviceToHost, g->stream));
+    GR_CUDA(cudaMemsetAsync(&g->ctl->sticky, 0, sizeof(unsigned long long), g->stream));
     GR_CUDA(cudaStreamSynchronize(g->stream));
     g->stats_levels = (int)levels;
     g->stats_records = (int)(levels < (unsigned long long)kMaxStatRecords ? levels : kMaxStatRecords);
@@ -112,26 +113,37 @@ gr_status gr_graph_info_get(const gr_graph *h, gr_graph_info *out) {
     return GR_OK;
 }
 
-gr_status gr_bfs(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts *opts) {
-    g_err[0] = 0;
+static gr_status bfs_args(gr_graph *h, int32_t src, const int32_t *depth_out, const gr_bfs_opts *opts,
+                          gr_bfs_opts *o) {
     if (!h || !depth_out) { set_error("graph or depth_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     Graph *g = (Graph *)h;
     if (src < 0 || src >= g->n) {
         set_error("src=%d not in [0, n=%lld)", src, (long long)g->n);
         return GR_ERR_OUT_OF_RANGE;
     }
-    gr_bfs_opts o{};
-    if (opts) o = *opts;
-    if (o.direction < 0 || o.direction > 2 || o.strategy < 0 || o.strategy > 2 || o.switch_rule < 0 ||
-        o.switch_rule > 1 || o.idempotent < 0 || o.idempotent > 1 || o.alpha < 0 || o.beta < 0) {
+    *o = gr_bfs_opts{};
+    if (opts) *o = *opts;
+    if (o->direction < 0 || o->direction > 2 || o->strategy < 0 || o->strategy > 2 || o->switch_rule < 0 ||
+        o->switch_rule > 1 || o->idempotent < 0 || o->idempotent > 1 || o->alpha < 0 || o->beta < 0) {
         set_error("invalid gr_bfs_opts");
         return GR_ERR_INVALID_ARGUMENT;
     }
     GR_CUDA(cudaSetDevice(g->device));
+    return GR_OK;
+}
+
+gr_status gr_graph_sync(gr_graph *h);
+
+gr_status gr_bfs(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts *opts) {
+    g_err[0] = 0;
+    gr_bfs_opts o;
+    gr_status st = bfs_args(h, src, depth_out, opts, &o);
+    if (st != GR_OK) return st;
+    Graph *g = (Graph *)h;
+    if (g->pending && (st = gr_graph_sync(h)) != GR_OK) return st;
     const bool dev_depth = ptr_on_device(depth_out);
     const bool dev_pred = pred_out && ptr_on_device(pred_out);
     int32_t *depth = depth_out, *pred = pred_out;
-    gr_status st;
     if (!dev_depth) {
         if ((st = ensure(g, (void **)&g->depth_buf, g->n * sizeof(int32_t))) != GR_OK) return st;
         depth = g->depth_buf;
@@ -163,8 +175,33 @@ gr_status gr_bfs(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out
     return st;
 }
 
-gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_out, const gr_sssp_opts *opts) {
+gr_status gr_bfs_async(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out,
+                       const gr_bfs_opts *opts) {
     g_err[0] = 0;
+    gr_bfs_opts o;
+    gr_status st = bfs_args(h, src, depth_out, opts, &o);
+    if (st != GR_OK) return st;
+    Graph *g = (Graph *)h;
+    if (!ptr_on_device(depth_out) || (pred_out && !ptr_on_device(pred_out))) {
+        set_error("gr_bfs_async needs device output buffers");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    int launches = 0;
+    if ((st = run_bfs(g, src, depth_out, pred_out, o, &launches)) != GR_OK) return st;
+    GR_CUDA(cudaGetLastError());
+    g->last_launches = launches;
+    g->last_delta = 0;
+    g->pending++;
+    g->pending_kind = 1;
+    g->pending_src = src;
+    g->pending_out[0] = depth_out;
+    g->pending_out[1] = pred_out;
+    g->pending_bopts = o;
+    return GR_OK;
+}
+
+static gr_status sssp_args(gr_graph *h, int32_t src, const uint32_t *dist_out, const gr_sssp_opts *opts,
+                           uint64_t *delta_out) {
     if (!h || !dist_out) { set_error("graph or dist_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     Graph *g = (Graph *)h;
     if (!g->has_w) { set_error("graph was created without weights"); return GR_ERR_NO_WEIGHTS; }
@@ -191,6 +228,7 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
         delta = avg >= 8.0 ? (mw + 10) / 21 : mw * 32;
         if (delta == 0) delta = 1;
     }
+    *delta_out = delta;
     GR_CUDA(cudaSetDevice(g->device));
     gr_status st;
     if ((st = ensure(g, (void **)&g->dp, g->n * sizeof(unsigned long long))) != GR_OK) return st;
@@ -200,6 +238,16 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
         if ((st = dev_alloc(g, (void **)&g->farq[0], g->far_cap * sizeof(int32_t))) != GR_OK) return st;
         if ((st = dev_alloc(g, (void **)&g->farq[1], g->far_cap * sizeof(int32_t))) != GR_OK) return st;
     }
+    return GR_OK;
+}
+
+gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_out, const gr_sssp_opts *opts) {
+    g_err[0] = 0;
+    uint64_t delta = 0;
+    gr_status st = sssp_args(h, src, dist_out, opts, &delta);
+    if (st != GR_OK) return st;
+    Graph *g = (Graph *)h;
+    if (g->pending && (st = gr_graph_sync(h)) != GR_OK) return st;
     const bool dev_dist = ptr_on_device(dist_out);
     const bool dev_pred = pred_out && ptr_on_device(pred_out);
     uint32_t *dist = dist_out;
@@ -221,6 +269,58 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
     g->last_launches = launches;
     g->last_delta = (uint32_t)(delta > 0xFFFFFFFFull ? 0xFFFFFFFFull : delta);
     return finish_run(g);
+}
+
+gr_status gr_sssp_async(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_out,
+                        const gr_sssp_opts *opts) {
+    g_err[0] = 0;
+    uint64_t delta = 0;
+    gr_status st = sssp_args(h, src, dist_out, opts, &delta);
+    if (st != GR_OK) return st;
+    Graph *g = (Graph *)h;
+    if (!ptr_on_device(dist_out) || (pred_out && !ptr_on_device(pred_out))) {
+        set_error("gr_sssp_async needs device output buffers");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    int launches = 0;
+    if ((st = run_sssp(g, src, dist_out, pred_out, delta, &launches)) != GR_OK) return st;
+    GR_CUDA(cudaGetLastError());
+    g->last_launches = launches;
+    g->last_delta = (uint32_t)(delta > 0xFFFFFFFFull ? 0xFFFFFFFFull : delta);
+    g->pending++;
+    g->pending_kind = 2;
+    g->pending_src = src;
+    g->pending_out[0] = dist_out;
+    g->pending_out[1] = pred_out;
+    return GR_OK;
+}
+
+gr_status gr_graph_sync(gr_graph *h) {
+    if (!h) { set_error("graph is NULL"); return GR_ERR_INVALID_ARGUMENT; }
+    Graph *g = (Graph *)h;
+    GR_CUDA(cudaSetDevice(g->device));
+    unsigned long long sticky = 0;
+    GR_CUDA(cudaMemcpyAsync(&sticky, &g->ctl->sticky, sizeof(sticky), cudaMemcpyDeviceToHost, g->stream));
+    const int np = g->pending;
+    g->pending = 0;
+    gr_status st = finish_run(g);  // synchronises; stats of the last run; clears sticky
+    if (np == 0) return GR_OK;
+    if (st == GR_OK && sticky) {
+        set_error("a frontier queue exceeded its capacity in one of %d asynchronous runs", np);
+        st = GR_ERR_OVERFLOW;
+    }
+    if (st == GR_ERR_OVERFLOW && np == 1 && g->pending_kind == 1 && g->pending_bopts.idempotent) {
+        // the one pending idempotent BFS overflowed: redo it with exactly-once claims
+        gr_bfs_opts o = g->pending_bopts;
+        o.idempotent = 0;
+        int launches = 0;
+        if ((st = run_bfs(g, g->pending_src, (int32_t *)g->pending_out[0], (int32_t *)g->pending_out[1], o,
+                          &launches)) != GR_OK)
+            return st;
+        g->last_launches += launches;
+        st = finish_run(g);
+    }
+    return st;
 }
 
 gr_status gr_get_run_stats(gr_graph *h, gr_run_stats *out) {

@@ -37,6 +37,16 @@ constexpr int kBfsStages = GR_BFS_STAGES;  // cp.async pipeline depth of the gri
 constexpr int kSmallCntBits = 24;   // count field of the small-mode packed counter
 constexpr unsigned long long kSmallCntMask = (1ull << kSmallCntBits) - 1;
 
+constexpr int kPullList = 96;   // pull: per-warp candidate list (< 64 + 32 before a batch)
+#ifndef GR_PULL_GRAB
+#define GR_PULL_GRAB 4
+#endif
+constexpr int kPullGrab = GR_PULL_GRAB;  // pull: bitmap words per grab
+#ifndef GR_PULL_LONG
+#define GR_PULL_LONG 4
+#endif
+constexpr int64_t kPullLong = GR_PULL_LONG;  // pull: longer unresolved in-lists are scanned by the warp
+
 struct BfsArgs {
     int64_t n, m;
     const int64_t *R;
@@ -63,16 +73,22 @@ struct BfsArgs {
     int64_t small_f, small_e;  // small-mode thresholds (<= kSmallF, tuning knobs)
     int32_t strategy;          // 0 auto, 1 thread/warp/CTA, 2 merge-path (gr_bfs_opts)
     int64_t lb_threshold;      // auto: frontiers below it use thread/warp/CTA
+    int64_t sbm_words;         // words of the shared-memory bitmap snapshot (0: off)
+    int64_t snap_min_edges;    // push steps with at least this many frontier edges use it
+    int32_t lb_chunks;         // dynamic merge-path pieces per warp (0: static partition)
+    int32_t claim_cas;         // push claim: CAS on depth[] (1) or atomicOr on the bitmap (0)
 };
 
-struct BfsSmem {
+template <int kNW>
+struct BfsSmemT {
     union {
         struct {  // grid levels: per-warp append staging + cp.async pipeline
-            PipeWarpSmem<(kBfsStages > 0 ? kBfsStages : 1), false> pipe[kBfsStages > 0 ? kWarpsPerBlock : 1];
-            int32_t sv[kWarpsPerBlock][kStageCap];
-            int32_t sd[kWarpsPerBlock][kStageCap];
-            int64_t sr[kWarpsPerBlock][kStageCap];
+            PipeWarpSmem<(kBfsStages > 0 ? kBfsStages : 1), false> pipe[kBfsStages > 0 ? kNW : 1];
+            int32_t sv[kNW][kStageCap];
+            int32_t sd[kNW][kStageCap];
+            int64_t sr[kNW][kStageCap];
         } stage;
+        int32_t plist[kNW][kPullList];  // pull steps: per-warp candidate lists
         struct {  // small mode: the frontier lives here (double-buffered)
             int64_t rs[2][kSmallF];   // row start of each entry
             int64_t off[2][kSmallF];  // exclusive degree prefix (reserved at append time)
@@ -80,8 +96,8 @@ struct BfsSmem {
         } small;
     } u;
     unsigned long long ctl[8];
-    long long scan[kWarpsPerBlock];
-    unsigned long long bsum[4];
+    long long scan[kNW];
+    unsigned long long bsum[6];
     unsigned long long pk[3];   // small mode: packed (edges << kSmallCntBits) | count, per level mod 3
     unsigned long long nd[3];   // small mode: discovered per level mod 3
     int work;
@@ -115,6 +131,9 @@ struct BfsPushOp {
                          // directly: one L2 round trip less on the critical path),
                          // 1 L2-coherent, 2 through L1 (most targets already visited
                          // before the level: L1 hits, stale words only cost an atomic)
+    int claim_cas;       // non-idempotent claim by CAS on depth (1) or atomicOr on the bitmap (0)
+    uint32_t sbm;        // shared address of the visited snapshot (targets < sbits)
+    int64_t sbits;       // 0: no snapshot this step
 
     __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
 
@@ -125,6 +144,7 @@ struct BfsPushOp {
 #pragma unroll
         for (int u = 0; u < U; ++u)
             word[u] = !ok[u] ? 0xffffffffu
+                    : dst[u] < sbits ? lds_u32(sbm + 4u * (uint32_t)(dst[u] >> 5))
                     : probe == 1 ? ld_probe(visited + (dst[u] >> 5), pol_keep)
                     : probe == 2 ? ld_l1(visited + (dst[u] >> 5)) : 0u;
         bool disc[U];
@@ -134,6 +154,10 @@ struct BfsPushOp {
             const uint32_t bit = 1u << (w & 31);
             disc[u] = false;
             bool cand = ok[u] && !(word[u] & bit);
+            // snapshot: the first warp of this CTA to reach w sets its bit in
+            // shared memory; the CTA's later visitors of w stop here (culling
+            // inside the CTA is exact; the global claim below stays the truth)
+            if (cand && w < sbits) cand = !(atom_or_shared(sbm + 4u * (uint32_t)(w >> 5), bit) & bit);
             if (idempotent) {
                 // warp-level culling heuristic (A-5 i): lanes of one warp that
                 // target the same vertex keep only the lowest lane
@@ -146,6 +170,11 @@ struct BfsPushOp {
                         disc[u] = true;
                         atomicOr(visited + (w >> 5), bit);  // result unused -> RED.OR
                     }
+                } else if (claim_cas) {
+                    // exactly-once per VERTEX: contention only between claims of
+                    // the same vertex, not of the 32 vertices sharing a bitmap word
+                    disc[u] = atomicCAS(depth + w, -1, next_depth) == -1;
+                    if (disc[u]) atomicOr(visited + (w >> 5), bit);  // RED.OR
                 } else {
                     const uint32_t old = atomicOr(visited + (w >> 5), bit);
                     disc[u] = !(old & bit);
@@ -248,104 +277,190 @@ struct SmallPushOp {
 // Pull (bottom-up) step over in-edges: "pull starts with a
 // frontier of unvisited vertices, generating the new frontier by filtering
 // the unvisited frontier for vertices that have neighbors in the current
-// frontier"; the current frontier is held as a bitmap. A warp
-// owns 32 consecutive vertices = one bitmap word, so the next-frontier word
-// and the visited word are written with one plain store from a ballot: no
-// atomics. Each lane stops at its first in-neighbour in the frontier (early
-// exit). Each CTA owns a contiguous range of words; its warps take words from
-// a shared-memory counter (per-vertex scan lengths vary widely).
+// frontier"; the current frontier is held as a bitmap.
+// B200 design: each CTA owns a contiguous range of visited-bitmap words; its
+// warps take 16 words at a time and COMPACT the unvisited vertices of those
+// words into a per-warp shared-memory list (filter of the unvisited set, one
+// ballot per round), so every lane of a batch works on a real candidate (a
+// late pull step has ~1 candidate per 10 vertices: a lane-per-vertex sweep
+// would leave 90% of the lanes idle through the whole dependent chain
+// R' -> C' -> frontier bit). A batch is 64 candidates, two per lane, with
+// the loads of both issued back to back. Each candidate stops at its first
+// in-neighbour in the frontier (early exit; in-lists are ordered by neighbour
+// degree, so hubs come first). Found vertices set their bits in the next
+// frontier and visited bitmaps with fire-and-forget RED.OR.
+// The next frontier is kept as a bitmap only ("lazy queue"): the step counts
+// its size and edges (for the direction rule) and a following push step
+// builds the queue from the bitmap (bitmap_to_queue), so pull -> pull
+// sequences never write a queue.
 // ---------------------------------------------------------------------------
+
+struct PullCounts {
+    unsigned long long ndisc = 0, insp = 0, qcnt = 0, qedges = 0;
+    unsigned dmax = 0;
+};
+
 __device__ __forceinline__ void pull_level(const BfsArgs &a, const uint32_t *__restrict__ fcur,
-                                           uint32_t *__restrict__ fnext, int32_t next_depth,
-                                           int *swork, Appender &app, unsigned long long &ndisc,
-                                           unsigned long long &insp) {
+                                           uint32_t *__restrict__ fnext, int32_t next_depth, int *swork,
+                                           int32_t *wl, PullCounts &pc, uint32_t sbm, int64_t sbits) {
     const int64_t nwords = (a.n + 31) / 32;
     const int64_t wb0 = nwords * blockIdx.x / gridDim.x;
     const int64_t wb1 = nwords * (blockIdx.x + 1) / gridDim.x;
     const unsigned l = lane_id();
     const unsigned long long pol = policy_evict_first();
     const bool sym = a.Rt == a.R;
-    // kPW words per grab, processed in phases so their loads overlap: row
-    // offsets of all kPW vertices, then their FIRST in-neighbour and its
-    // frontier bit (most candidates resolve there: C2 averages 1.8 inspected
-    // edges per candidate), then the remaining lists of the unresolved ones.
-#ifndef GR_PULL_WORDS
-#define GR_PULL_WORDS 2
-#endif
-    constexpr int kPW = GR_PULL_WORDS;
-    for (;;) {
-        int c = 0;
-        if (l == 0) c = atomicAdd(swork, kPW);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        const int64_t w0 = wb0 + c;
-        if (w0 >= wb1) break;
-        uint32_t visw[kPW];
-        int64_t beg[kPW], end[kPW];
-        int32_t parent[kPW];
-        bool found[kPW];
+    const uint32_t tail = (a.n & 31) ? ((1u << (a.n & 31)) - 1u) : 0xffffffffu;
+    auto fbit = [&](int32_t u) -> bool {
+        const uint32_t fw = u < sbits ? lds_u32(sbm + 4u * (uint32_t)(u >> 5)) : __ldg(fcur + (u >> 5));
+        return (fw >> (u & 31)) & 1u;
+    };
+    int cnt = 0;  // warp-uniform
+    auto process = [&](int k) {  // candidates wl[0, k), k <= 64
+        int32_t v[2], par[2], u0[2];
+        int64_t beg[2], end[2];
+        bool fnd[2];
 #pragma unroll
-        for (int k = 0; k < kPW; ++k) visw[k] = (w0 + k < wb1) ? a.visited[w0 + k] : 0xffffffffu;
+        for (int q = 0; q < 2; ++q) v[q] = ((int)l + 32 * q < k) ? wl[l + 32 * q] : -1;
 #pragma unroll
-        for (int k = 0; k < kPW; ++k) {
-            const int64_t v = (w0 + k) * 32 + l;
-            const bool cand = v < a.n && !((visw[k] >> l) & 1u);
-            beg[k] = cand ? a.Rt[v] : 0;
-            end[k] = cand ? a.Rt[v + 1] : 0;
-        }
-        int32_t u0[kPW];
-#pragma unroll
-        for (int k = 0; k < kPW; ++k) u0[k] = beg[k] < end[k] ? ld_stream(a.Ct + beg[k], pol) : -1;
-#pragma unroll
-        for (int k = 0; k < kPW; ++k) {
-            const uint32_t fw = u0[k] >= 0 ? __ldg(fcur + (u0[k] >> 5)) : 0u;
-            found[k] = u0[k] >= 0 && ((fw >> (u0[k] & 31)) & 1u);
-            parent[k] = u0[k];
-            insp += (u0[k] >= 0);
+        for (int q = 0; q < 2; ++q) {
+            beg[q] = v[q] >= 0 ? a.Rt[v[q]] : 0;
+            end[q] = v[q] >= 0 ? a.Rt[v[q] + 1] : 0;
         }
 #pragma unroll
-        for (int k = 0; k < kPW; ++k) {
-            if (found[k]) continue;
-            for (int64_t e = beg[k] + 1; e < end[k] && !found[k]; e += 4) {
+        for (int q = 0; q < 2; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Ct + beg[q], pol) : -1;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            fnd[q] = u0[q] >= 0 && fbit(u0[q]);
+            par[q] = u0[q];
+            pc.insp += (u0[q] >= 0);
+        }
+        // the rest of each unresolved list: first by its lane (4 edges a step,
+        // at most kPullLong edges), then what is left of the long ones by the
+        // whole warp, 32 edges a step with a ballot early exit (one lane
+        // scanning a long list alone held its warp for 100+ us on C3)
+        int64_t nxt[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            nxt[q] = beg[q] + 1;
+            if (fnd[q]) continue;
+            const int64_t lim = (end[q] - nxt[q] > kPullLong) ? nxt[q] + kPullLong : end[q];
+            for (int64_t e = nxt[q]; e < lim && !fnd[q]; e += 4) {
                 int32_t u[4];
-                uint32_t fw[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) u[q] = (e + q < end[k]) ? ld_stream(a.Ct + e + q, pol) : -1;
+                for (int j = 0; j < 4; ++j) u[j] = (e + j < lim) ? ld_stream(a.Ct + e + j, pol) : -1;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) fw[q] = (u[q] >= 0) ? __ldg(fcur + (u[q] >> 5)) : 0u;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    if (!found[k] && u[q] >= 0) {
-                        ++insp;
-                        if ((fw[q] >> (u[q] & 31)) & 1u) {
-                            found[k] = true;
-                            parent[k] = u[q];
-                        }
+                for (int j = 0; j < 4; ++j) {
+                    if (!fnd[q] && u[j] >= 0) {
+                        ++pc.insp;
+                        if (fbit(u[j])) { fnd[q] = true; par[q] = u[j]; }
                     }
                 }
             }
+            nxt[q] = lim;
+        }
+        bool lng[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) lng[q] = !fnd[q] && nxt[q] < end[q];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            unsigned lm = __ballot_sync(0xffffffffu, lng[q]);
+            while (lm) {
+                const int ld = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const int64_t b = __shfl_sync(0xffffffffu, nxt[q], ld);
+                const int64_t e = __shfl_sync(0xffffffffu, end[q], ld);
+                int32_t hitu = -1;
+                for (int64_t x = b; x < e; x += 32) {
+                    const int32_t u = (x + l < e) ? ld_stream(a.Ct + x + l, pol) : -1;
+                    const bool hit = u >= 0 && fbit(u);
+                    const unsigned bm = __ballot_sync(0xffffffffu, hit);
+                    const int first = bm ? __ffs(bm) - 1 : 32;
+                    pc.insp += (u >= 0 && (int)l <= first);
+                    if (bm) {
+                        hitu = __shfl_sync(0xffffffffu, u, first);
+                        break;
+                    }
+                }
+                if ((int)l == ld && hitu >= 0) { fnd[q] = true; par[q] = hitu; }
+            }
         }
 #pragma unroll
-        for (int k = 0; k < kPW; ++k) {
-            const int64_t wi = w0 + k;
-            if (wi >= wb1) break;
-            const int64_t v = wi * 32 + l;
-            const unsigned nb = __ballot_sync(0xffffffffu, found[k]);
-            if (l == 0) {
-                fnext[wi] = nb;
-                if (nb) a.visited[wi] = visw[k] | nb;
+        for (int q = 0; q < 2; ++q) {
+            if (!fnd[q]) continue;
+            const int32_t x = v[q];
+            a.depth[x] = next_depth;
+            if (a.pred) a.pred[x] = par[q];
+            const uint32_t bit = 1u << (x & 31);
+            atomicOr(fnext + (x >> 5), bit);      // RED.OR
+            atomicOr(a.visited + (x >> 5), bit);  // RED.OR
+            const int64_t deg = sym ? end[q] - beg[q] : a.R[x + 1] - a.R[x];
+            ++pc.ndisc;
+            if (deg > 0) {
+                ++pc.qcnt;
+                pc.qedges += (unsigned long long)deg;
+                pc.dmax = max(pc.dmax, (unsigned)deg);
             }
-            if (nb == 0) continue;
-            int64_t deg = 0, rs = 0;
-            if (found[k]) {
-                a.depth[v] = next_depth;
-                if (a.pred) a.pred[v] = parent[k];
-                rs = sym ? beg[k] : a.R[v];
-                deg = sym ? end[k] - beg[k] : a.R[v + 1] - rs;
-            }
-            ndisc += found[k];
-            app.push(found[k] && deg > 0, (int32_t)v, deg, rs);
+        }
+        // keep the unprocessed tail (cnt - k < 32 entries) at the front
+        __syncwarp();
+        const int rem = cnt - k;
+        const int32_t t = ((int)l < rem) ? wl[k + l] : 0;
+        __syncwarp();
+        if ((int)l < rem) wl[l] = t;
+        __syncwarp();
+        cnt = rem;
+    };
+    for (;;) {
+        int c = 0;
+        if (l == 0) c = atomicAdd(swork, kPullGrab);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const int64_t w0 = wb0 + c;
+        if (w0 >= wb1) break;
+        const int64_t wi = w0 + l;
+        uint32_t cm = ((int)l < kPullGrab && wi < wb1) ? ~a.visited[wi] : 0u;
+        if (wi == nwords - 1) cm &= tail;
+        // word by word, lane b takes bit b: the list stays sorted by vertex id,
+        // so a batch's depth/pred stores and bitmap REDs touch few lines
+        unsigned nz = __ballot_sync(0xffffffffu, cm != 0);
+        while (nz) {
+            const int j = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t w = __shfl_sync(0xffffffffu, cm, j);
+            if ((w >> l) & 1u) wl[cnt + __popc(w & lanemask_lt())] = (int32_t)((w0 + j) * 32 + l);
+            cnt += __popc(w);
+            __syncwarp();
+            if (cnt >= 64) process(64);
         }
     }
+    while (cnt > 0) process(cnt < 64 ? cnt : 64);
+}
+
+// Frontier bitmap -> queue (the other direction of the
+// conversion): the frontier of a pull step, needed as a queue when the next
+// step pushes. Warp-strided over 32-word chunks; appends (v, degree prefix,
+// R[v]) for every set bit with out-degree > 0.
+template <class App>
+__device__ __forceinline__ void bitmap_to_queue(const BfsArgs &a, const uint32_t *__restrict__ fb,
+                                                int64_t gw, int64_t nw, App &app) {
+    const int64_t nwords = (a.n + 31) / 32;
+    const unsigned l = lane_id();
+    for (int64_t w0 = gw * 32; w0 < nwords; w0 += nw * 32) {
+        const int64_t wi = w0 + l;
+        uint32_t bits = wi < nwords ? __ldcg(fb + wi) : 0u;
+        while (__any_sync(0xffffffffu, bits != 0)) {
+            const bool has = bits != 0;
+            int32_t v = 0;
+            int64_t rs = 0, deg = 0;
+            if (has) {
+                v = (int32_t)(wi * 32 + (__ffs(bits) - 1));
+                bits &= bits - 1;
+                rs = a.R[v];
+                deg = a.R[v + 1] - rs;
+            }
+            app.push(has && deg > 0, v, deg, rs);
+        }
+    }
+    app.finish();
 }
 
 // Direction decision (reading A-3). Pure function of counters
@@ -372,6 +487,7 @@ struct BfsState {  // per-traversal heuristic state, identical in every CTA
     int fb_valid;       // fbuf[L%3] holds the frontier of level L
     int fbn_clean;      // fbuf[(L+1)%3] is all zero
     int closed;         // stats records below this level are closed
+    int q_valid;        // the queue of level L is materialised (a pull step keeps a bitmap only)
 };
 
 __device__ __forceinline__ long long gtimer() {
@@ -380,29 +496,19 @@ __device__ __forceinline__ long long gtimer() {
     return t;
 }
 
-// Block-wide exclusive scan of one int64 per thread; returns the exclusive
-// prefix, total in *total. Uses s->scan; contains two __syncthreads.
-__device__ __forceinline__ int64_t block_excl_scan(int64_t x, int64_t *total, BfsSmem *s) {
-    const int wib = threadIdx.x >> 5;
-    const int64_t incl = warp_incl_scan<int64_t>(x);
-    __syncthreads();  // s->scan / s->bsum[3] may still be read by a previous scan
-    if (lane_id() == 31) s->scan[wib] = incl;
-    __syncthreads();
-    if (wib == 0) {
-        const int64_t y = (lane_id() < kWarpsPerBlock) ? s->scan[lane_id()] : 0;
-        const int64_t yi = warp_incl_scan<int64_t>(y);
-        if (lane_id() < kWarpsPerBlock) s->scan[lane_id()] = yi - y;
-        if (lane_id() == 31) s->bsum[3] = (unsigned long long)yi;
-    }
-    __syncthreads();
-    *total = (int64_t)s->bsum[3];
-    return s->scan[wib] + incl - x;
-}
+template <int kBlk>
+__host__ __device__ constexpr size_t bfs_sbm_offset() { return (sizeof(BfsSmemT<kBlk / kWarp>) + 127) & ~(size_t)127; }
 
-__global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
+template <int kBlk, int kMinB>
+__global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
+    constexpr int kNW = kBlk / kWarp;
+    using BfsSmem = BfsSmemT<kNW>;
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     BfsSmem *s = reinterpret_cast<BfsSmem *>(smem_raw);
+    uint32_t *sbm_p = reinterpret_cast<uint32_t *>(smem_raw + bfs_sbm_offset<kBlk>());
+    const uint32_t sbm = (uint32_t)__cvta_generic_to_shared(sbm_p);
+    const int64_t sbits = a.sbm_words * 32;
 
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
@@ -432,6 +538,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         a.qo[0][0] = 0;
         a.qr[0][0] = a.R[a.src];
         a.ctl->slot[0].qpack = (deg_src > 0) ? (((unsigned long long)deg_src << a.S) | 1ull) : 0ull;
+        a.ctl->slot[0].dmax = (unsigned long long)deg_src;
     }
     grid.sync();
 
@@ -448,6 +555,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
     st.fb_valid = 0;
     st.fbn_clean = 0;
     st.closed = 0;
+    st.q_valid = 1;
     const unsigned long long pol_keep = policy_evict_last();
     long long t_prev = 0;
     if (tid == 0) t_prev = gtimer();
@@ -469,15 +577,20 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
             const Slot &cur = a.ctl->slot[L & 3];
             // independent relaxed loads: issued back to back, one round trip
             const unsigned long long q0 = ld_relaxed(&cur.qpack), q1 = ld_relaxed(&cur.ndisc),
-                                     q2 = ld_relaxed(&cur.insp), q3 = ld_relaxed(&a.ctl->overflow);
-            s->ctl[0] = q0; s->ctl[1] = q1; s->ctl[2] = q2; s->ctl[3] = q3;
+                                     q2 = ld_relaxed(&cur.insp), q3 = ld_relaxed(&a.ctl->overflow),
+                                     q4 = ld_relaxed(&cur.dmax);
+            s->ctl[0] = q0; s->ctl[1] = q1; s->ctl[2] = q2; s->ctl[3] = q3; s->ctl[4] = q4;
             // per-level CTA counters, reset before the barrier below (racecheck)
-            s->work = 0; s->bsum[0] = 0; s->bsum[1] = 0;
+            s->work = 0; s->bsum[0] = 0; s->bsum[1] = 0; s->bsum[4] = 0; s->bsum[5] = 0;
+#ifdef GR_TRACE
+            s->bsum[2] = ~0ull; s->bsum[3] = 0;
+#endif
         }
         __syncthreads();
         const unsigned long long qp = s->ctl[0];
         const int64_t f = (int64_t)(qp & cmask);
         const int64_t mf = (int64_t)(qp >> a.S);
+        const int64_t dmax = (int64_t)s->ctl[4];
         if (pending) {
             st.u_cnt -= (int64_t)s->ctl[1];
             st.m_u -= mf;
@@ -495,12 +608,24 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         __syncthreads();  // s->ctl is rewritten below
         if (stop) break;
         const int dir = decide_direction(a, st.dir, f, mf, st.u_cnt, st.m_u, st.prev_f, nwords);
+        if (dir == 1 && !st.q_valid) {
+            // the frontier of the last pull step exists as a bitmap only
+            Appender conv = app;
+            Slot &cs = a.ctl->slot[L & 3];
+            conv.qv = a.qv[L & 1]; conv.qo = a.qo[L & 1]; conv.qr = a.qr[L & 1];
+            conv.counter = &cs.fpack;
+            conv.dmax = nullptr;
+            conv.cnt = 0;
+            bitmap_to_queue(a, a.fbuf[L % 3], gw, nw, conv);
+            grid.sync();
+            st.q_valid = 1;
+        }
 
         if (dir == 1 && f <= a.small_f && mf <= a.small_e) {
             // ================= small mode: CTA 0 alone ===========================
             if (blockIdx.x == 0) {
                 int c = 0, r = 0;
-                for (int64_t j = threadIdx.x; j < f; j += kBlock) {
+                for (int64_t j = threadIdx.x; j < f; j += kBlk) {
                     const int32_t v = a.qv[L & 1][j];
                     s->u.small.q[0][j] = v;
                     s->u.small.off[0][j] = a.qo[L & 1][j];
@@ -539,7 +664,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                                    a.qv[(Lc + 1) & 1], a.qo[(Lc + 1) & 1], a.qr[(Lc + 1) & 1], 0ull};
                     SmemFrontier fr{s->u.small.q[c], s->u.small.off[c], s->u.small.rs[c], cf, E};
                     GR_TSTAMP(9);
-                    expand_lb(fr, a.C, (int64_t)wib, (int64_t)kWarpsPerBlock, op);
+                    expand_lb(fr, a.C, (int64_t)wib, (int64_t)kNW, op);
                     GR_TSTAMP(5);
                     const unsigned long long ndw = warp_sum<unsigned long long>(op.ndisc);
                     if (lane_id() == 0 && ndw) atomicAdd(&s->nd[r1], ndw);
@@ -567,7 +692,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                 if (!done) {
                     // the frontier of level st.L: entries below kSmallF are in shared
                     // memory, the rest were spilled (with their offsets) to the global queue
-                    for (int64_t j = threadIdx.x; j < cf && j < kSmallF; j += kBlock) {
+                    for (int64_t j = threadIdx.x; j < cf && j < kSmallF; j += kBlk) {
                         a.qv[st.L & 1][j] = s->u.small.q[c][j];
                         a.qo[st.L & 1][j] = s->u.small.off[c][j];
                         a.qr[st.L & 1][j] = s->u.small.rs[c][j];
@@ -577,6 +702,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                         a.ctl->slot[st.L & 3].qpack = ((unsigned long long)E << a.S) | (unsigned long long)cf;
                         a.ctl->slot[st.L & 3].ndisc = 0;
                         a.ctl->slot[st.L & 3].insp = 0;
+                        a.ctl->slot[st.L & 3].work = 0;
+                        a.ctl->slot[st.L & 3].dmax = (unsigned long long)E;  // bound: max deg <= E
                     }
                 } else if (threadIdx.x == 0) {
                     a.ctl->slot[st.L & 3].qpack = 0;
@@ -584,7 +711,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
                 if (threadIdx.x == 0) {
                     for (int k = 1; k <= 2; ++k) {
                         Slot &r = a.ctl->slot[(st.L + k) & 3];
-                        r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull;
+                        r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull; r.dmax = 0;
                     }
                     long long *bs = a.ctl->bstate;
                     bs[0] = st.L; bs[1] = st.dir; bs[2] = st.prev_dir; bs[3] = st.u_cnt;
@@ -607,6 +734,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
             st.closed = st.L;      // records below st.L are closed
             st.fb_valid = 0;       // small mode keeps no frontier bitmap
             st.fbn_clean = 0;
+            st.q_valid = 1;
             pending = false;
             __syncthreads();
             continue;
@@ -621,6 +749,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         if (tid == 0) {
             Slot &rst = a.ctl->slot[(L + 2) & 3];
             rst.qpack = 0; rst.ndisc = 0; rst.fpack = 0; rst.work = 0; rst.minfar = ~0ull; rst.insp = 0;
+            rst.dmax = 0;
             if (L < kMaxStatRecords) {
                 gr_level_stats &sr = a.stats[L];
                 sr.level = L; sr.direction = dir; sr.frontier = f; sr.frontier_edges = mf;
@@ -632,6 +761,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         app.qo = a.qo[(L + 1) & 1];
         app.qr = a.qr[(L + 1) & 1];
         app.counter = &nxt.qpack;
+        app.dmax = &nxt.dmax;
         uint32_t *fb_c = a.fbuf[L % 3];
         uint32_t *fb_n = a.fbuf[(L + 1) % 3];
         uint32_t *fb_z = a.fbuf[(L + 2) % 3];
@@ -654,32 +784,60 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         const bool need_fb = (dir == 2) || (mf >= nwords / 4);
         if (need_fb)
             for (int64_t w = tid; w < nwords; w += nthreads) fb_z[w] = 0u;
+        const bool snap = a.sbm_words > 0 && (dir == 2 || mf >= a.snap_min_edges);
+        if (snap) {
+            // bitmap snapshot for this step: visited (push culling) or the
+            // current frontier (pull probes); read-only global state now
+            snapshot_bits(sbm_p, dir == 1 ? a.visited : fb_c, a.sbm_words);
+            __syncthreads();
+        }
         if (dir == 1) {
             BfsPushOp op{a.visited, st.fbn_clean ? fb_n : nullptr, a.depth, a.pred, a.R, L + 1,
                          a.idempotent, &app, 0ull, pol_keep,
-                         mf < (1 << 16) ? 0 : (st.m_u * 4 < a.m ? 2 : 1)};
+                         mf < (1 << 16) ? 0 : (snap || st.m_u * 4 >= a.m ? 1 : 2), a.claim_cas, sbm,
+                         snap ? sbits : 0};
             GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.qr[L & 1], f, mf};
             // auto (reading A-4, measured on B200): node-granular thread/warp/CTA
             // when the frontier's lists are short on average (mesh-like levels:
             // no frontier-wide search, 35% faster per level on C4); merge-path
             // over edges when a few lists carry the edges (hubs: one CTA per list
             // would serialise them; C2 level 1 is 26% slower with TWC)
+            // ... but never with a long list in the frontier: thread/warp/CTA
+            // gives a whole list to one CTA (measured on C2: one hub in a
+            // frontier of 1.07M short lists held the level at 576 us vs 89 us median)
             const bool twc = a.strategy == 1 ||
-                             (a.strategy == 0 && f < a.lb_threshold && mf <= 16 * f);
+                             (a.strategy == 0 && f < a.lb_threshold && mf <= 16 * f && dmax <= kTwcMaxDeg);
             if (twc) {
                 expand_twc(fr, a.C, op, &s->win);
             } else {
 #if GR_BFS_STAGES > 0
             expand_pipe<kBfsStages, false>(fr, a.C, nullptr, gw, nw, op, &s->u.stage.pipe[wib]);
 #else
-            expand_lb(fr, a.C, gw, nw, op);
+            expand_lb(fr, a.C, gw, nw, op, a.lb_chunks > 0 ? &a.ctl->slot[L & 3].work : nullptr,
+                      a.lb_chunks);
 #endif
             }
             ndisc = op.ndisc;
             st.fb_valid = st.fbn_clean;
         } else {
-            pull_level(a, fb_c, fb_n, L + 1, &s->work, app, ndisc, insp);
+            if (!st.fbn_clean) {  // RED.OR targets must start at zero
+                for (int64_t w = tid; w < nwords; w += nthreads) fb_n[w] = 0u;
+                grid.sync();
+            }
+            PullCounts pc;
+            pull_level(a, fb_c, fb_n, L + 1, &s->work, s->u.plist[wib], pc, sbm, snap ? sbits : 0);
+            ndisc = pc.ndisc;
+            insp = pc.insp;
+            // lazy queue: only the size, edges and max degree of the next frontier
+            const unsigned long long qc = warp_sum<unsigned long long>(pc.qcnt);
+            const unsigned long long qe = warp_sum<unsigned long long>(pc.qedges);
+            const unsigned dm = __reduce_max_sync(0xffffffffu, pc.dmax);
+            if (lane_id() == 0) {
+                if (qc) atomicAdd(&s->bsum[4], (qe << a.S) | qc);
+                if (dm) atomicMax(&s->bsum[5], (unsigned long long)dm);
+            }
             st.fb_valid = 1;
+            st.q_valid = 0;
         }
         GR_TSTAMP(5);
         app.finish();
@@ -689,10 +847,23 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         if (lane_id() == 0) {
             if (ndisc) atomicAdd(&s->bsum[0], ndisc);
             if (insp) atomicAdd(&s->bsum[1], insp);
+#ifdef GR_TRACE
+            const unsigned long long tw = (unsigned long long)gtimer();
+            atomicMin(&s->bsum[2], tw);
+            atomicMax(&s->bsum[3], tw);
+#endif
         }
         __syncthreads();
+#ifdef GR_TRACE
+        if (g_bal && threadIdx.x == 0 && L < 64) {
+            g_bal[((int64_t)L * gridDim.x + blockIdx.x) * 2] = (long long)s->bsum[2];
+            g_bal[((int64_t)L * gridDim.x + blockIdx.x) * 2 + 1] = (long long)s->bsum[3];
+        }
+#endif
         if (threadIdx.x == 0) {
             if (s->bsum[0]) atomicAdd(&nxt.ndisc, s->bsum[0]);
+            if (s->bsum[4]) atomicAdd(&nxt.qpack, s->bsum[4]);
+            if (s->bsum[5]) atomicMax(&nxt.dmax, s->bsum[5]);
             if (s->bsum[1]) atomicAdd(&nxt.insp, s->bsum[1]);
         }
         st.prev_dir = dir;
@@ -704,7 +875,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) bfs_kernel(BfsArgs a) {
         grid.sync();
         GR_TSTAMP(8);
     }
-    if (tid == 0) a.ctl->levels = (unsigned long long)st.L;
+    if (tid == 0) {
+        a.ctl->levels = (unsigned long long)st.L;
+        if (a.ctl->overflow) a.ctl->sticky = 1ull;
+    }
 }
 
 gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr_bfs_opts &o,
@@ -730,18 +904,43 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.S = g->pack_shift;
     a.small_f = env_int("GR_SMALL_F", kSmallFDefault);
     a.small_e = env_int("GR_SMALL_E", kSmallE);
+    a.lb_chunks = (int32_t)env_int("GR_LB_CHUNKS", 4);
+    a.claim_cas = (int32_t)env_int("GR_CLAIM_CAS", 0);
     if (a.small_f > kSmallF) a.small_f = kSmallF;
 
-    static int per_sm = 0;  // occupancy of the kernel (same on every device of the box)
-    const size_t smem = sizeof(BfsSmem);
-    if (per_sm == 0) {
-        GR_CUDA(cudaFuncSetAttribute(bfs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bfs_kernel, kBlock, smem));
+    // Kernel variant: graphs whose bitmap no
+    // longer fits in L1 run 1024-thread CTAs (1 per SM) with most of the
+    // shared memory holding a bitmap snapshot; small graphs keep 512 x 2 CTAs.
+    const int64_t nwords = (g->n + 31) / 32;
+    const bool use_snap = env_int("GR_SNAPSHOT", 0) != 0 && nwords * 4 > env_int("GR_SNAP_MIN_BYTES", 64 << 10);
+    static int optin = 0;
+    if (optin == 0) GR_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
+    const void *fn = use_snap ? (const void *)bfs_kernel<1024, 1> : (const void *)bfs_kernel<kBlock, kMinBlocks>;
+    const int block = use_snap ? 1024 : kBlock;
+    size_t smem;
+    a.sbm_words = 0;
+    a.snap_min_edges = env_int("GR_SNAP_MIN_EDGES", 1 << 20);
+    if (use_snap) {
+        const size_t off = bfs_sbm_offset<1024>();
+        int64_t w = ((int64_t)optin - (int64_t)off - 1024) / 4;  // 1 KB reserve
+        if (w > nwords) w = nwords;
+        a.sbm_words = w & ~3ll;
+        smem = off + (size_t)a.sbm_words * 4;
+    } else {
+        smem = sizeof(BfsSmemT<kBlock / kWarp>);
     }
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[use_snap]) {
+        GR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
+        attr_set[use_snap] = true;
+    }
+    int per_sm = 0;
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
     if (per_sm < 1) { set_error("bfs_kernel cannot be resident"); return GR_ERR_CUDA; }
-    dim3 grid(g->num_sms * per_sm), block(kBlock);
+    if (per_sm > (use_snap ? 1 : kMinBlocks)) per_sm = use_snap ? 1 : kMinBlocks;
+    dim3 grid(g->num_sms * per_sm), blk(block);
     void *args[] = {&a};
-    GR_CUDA(cudaLaunchCooperativeKernel((void *)bfs_kernel, grid, block, args, smem, g->stream));
+    GR_CUDA(cudaLaunchCooperativeKernel(fn, grid, blk, args, smem, g->stream));
     count_launch();
     *launches = 1;
     return GR_OK;
@@ -753,5 +952,9 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
 // debug only (not in gr.h): install the BFS level trace buffer (16 stamps x 256 levels)
 extern "C" int gr_debug_trace_set(long long *dev_buf) {
     return (int)cudaMemcpyToSymbol(gr::g_trace, &dev_buf, sizeof(dev_buf));
+}
+// debug only: per-level per-CTA [first, last] warp completion times (64 levels x grid x 2)
+extern "C" int gr_debug_balance_set(long long *dev_buf) {
+    return (int)cudaMemcpyToSymbol(gr::g_bal, &dev_buf, sizeof(dev_buf));
 }
 #endif

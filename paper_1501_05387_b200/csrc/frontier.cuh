@@ -31,6 +31,7 @@ namespace gr {
 #ifdef GR_TRACE
 static __device__ long long *g_trace;
 static __device__ int g_trace_L;
+static __device__ long long *g_bal;   // [64 levels][grid][2]: first / last warp done (per CTA)
 #define GR_TSTAMP(k)                                                                         \
     do {                                                                                    \
         if (g_trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_L < 256) {            \
@@ -65,24 +66,30 @@ struct AppenderT {
     int S;                          // count-field bits (offsets mode)
     int64_t cap;                    // queue capacity
     unsigned long long *overflow;
+    unsigned long long *dmax = nullptr;  // max appended degree (offsets mode; null: not tracked)
 
     __device__ __forceinline__ void flush() {
         const unsigned l = lane_id();
         const int k = cnt;
         constexpr int kR = kCap / 32;
-        int64_t incl[kR];
-        int64_t run = 0;
-#pragma unroll
-        for (int r = 0; r < kR; ++r) {
-            int64_t d = 0;
-            if (qo && r * 32 < k && r * 32 + (int)l < k) d = sd[r * 32 + l];
-            int64_t x = (qo && r * 32 < k) ? warp_incl_scan<int64_t>(d) : 0;
-            incl[r] = run + x - d;  // exclusive prefix of this entry
-            run += __shfl_sync(0xffffffffu, x, 31);
+        // pass 1: total degree (and max) of the staged entries
+        int64_t tot = 0;
+        unsigned mx = 0;
+        if (qo) {
+#pragma unroll 4
+            for (int r = 0; r < kR; ++r) {
+                const int j = r * 32 + (int)l;
+                const int64_t d = (j < k) ? (int64_t)sd[j] : 0;
+                tot += d;
+                mx = max(mx, (unsigned)d);
+            }
+            tot = warp_sum<int64_t>(tot);
+            if (dmax) mx = __reduce_max_sync(0xffffffffu, mx);
         }
         unsigned long long base = 0;
         if (l == 0) {
-            const unsigned long long add = qo ? (((unsigned long long)run << S) | (unsigned long long)k)
+            if (dmax && mx) atomicMax(dmax, (unsigned long long)mx);
+            const unsigned long long add = qo ? (((unsigned long long)tot << S) | (unsigned long long)k)
                                               : (unsigned long long)k;
             base = atomicAdd(counter, add);
         }
@@ -91,17 +98,22 @@ struct AppenderT {
         if ((int64_t)(cbase + k) > cap) {
             if (l == 0) atomicExch(overflow, 1ull);
         } else {
-            const int64_t ebase = (int64_t)(base >> S);
-#pragma unroll
+            // pass 2: exclusive degree prefix of each entry, then the writes
+            int64_t run = qo ? (int64_t)(base >> S) : 0;
+#pragma unroll 4
             for (int r = 0; r < kR; ++r) {
+                if (r * 32 >= k) break;
                 const int j = r * 32 + (int)l;
-                if (j < k) {
-                    qv[cbase + j] = sv[j];
-                    if (qo) {
-                        qo[cbase + j] = ebase + incl[r];
+                if (qo) {
+                    const int64_t d = (j < k) ? (int64_t)sd[j] : 0;
+                    const int64_t x = warp_incl_scan<int64_t>(d);
+                    if (j < k) {
+                        qo[cbase + j] = run + x - d;
                         qr[cbase + j] = sr[j];
                     }
+                    run += __shfl_sync(0xffffffffu, x, 31);
                 }
+                if (j < k) qv[cbase + j] = sv[j];
             }
         }
         __syncwarp();
@@ -168,6 +180,42 @@ __device__ __forceinline__ unsigned long long ld_probe(const unsigned long long 
     unsigned long long r;
     asm volatile("ld.global.cg.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(r) : "l"(p), "l"(pol));
     return r;
+}
+
+// Shared-memory bitmap snapshot: a prefix of a
+// global bitmap copied into shared memory at the start of a step, so the
+// per-edge random probes of the step are shared-memory loads (bank conflicts
+// only) instead of one 128-B L1TEX wavefront per distinct line.
+__device__ __forceinline__ uint32_t lds_u32(uint32_t saddr) {
+    uint32_t r;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(saddr));
+    return r;
+}
+__device__ __forceinline__ uint32_t atom_or_shared(uint32_t saddr, uint32_t v) {
+    uint32_t r;
+    asm volatile("atom.shared.or.b32 %0, [%1], %2;" : "=r"(r) : "r"(saddr), "r"(v) : "memory");
+    return r;
+}
+// CTA-wide copy of words [0, words) of src into sbm (words % 4 == 0).
+// The caller puts a __syncthreads() after it.
+__device__ __forceinline__ void snapshot_bits(uint32_t *sbm, const uint32_t *src, int64_t words) {
+    const int64_t n4 = words >> 2;
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    uint4 *d4 = reinterpret_cast<uint4 *>(sbm);
+    constexpr int U = 4;
+    for (int64_t i = threadIdx.x; i < n4; i += (int64_t)blockDim.x * U) {
+        uint4 v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int64_t j = i + (int64_t)k * blockDim.x;
+            if (j < n4) v[k] = __ldcg(s4 + j);
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int64_t j = i + (int64_t)k * blockDim.x;
+            if (j < n4) d4[j] = v[k];
+        }
+    }
 }
 
 // Smallest i in [0, F] with key(i) >= t, key non-decreasing, key(F) = +inf.
@@ -239,17 +287,15 @@ struct SmemFrontier {
 //   void edges<U>(ok[], src[], pay[], dst[], eidx[])  process U edges per lane
 // ---------------------------------------------------------------------------
 constexpr int kUnroll = 4;
+constexpr int64_t kMinChunk = 4096;           // dynamic merge-path: min items per piece
+constexpr int64_t kTwcMaxDeg = 4096;          // auto strategy: TWC only without longer lists
 constexpr int kGroup = 32 * kUnroll;          // edges per warp group
 
+// Processes the merged items [d0, d1) (d0 < d1).
 template <class Front, class Op>
-__device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__restrict__ C, int64_t gw,
-                                          int64_t nw, Op &op) {
+__device__ __forceinline__ void expand_lb_range(const Front &fr, const int32_t *__restrict__ C, int64_t d0,
+                                                int64_t d1, Op &op) {
     const int64_t F = fr.F, E = fr.E;
-    if (E <= 0 || F <= 0) return;
-    const int64_t D = F + E;
-    const int64_t d0 = (D * gw) / nw;  // D < 2^40, nw < 2^20: no overflow
-    const int64_t d1 = (D * (gw + 1)) / nw;
-    if (d0 >= d1) return;
     auto mkey = [&](int64_t i) { return fr.off(i) + i; };  // merged position of vertex i
     const int64_t i0 = warp_lower_bound(F, d0, mkey);
     const int64_t i1 = warp_lower_bound(F, d1, mkey);
@@ -329,6 +375,43 @@ __device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__rest
         }
         e = wend;
         i += 32;
+    }
+}
+
+// Static partition: warp gw of nw takes the gw-th equal piece of the merged
+// sequence. With `work` (a zeroed grid-wide counter): dynamic partition, the
+// merged sequence is cut into kChunks pieces per warp; warp gw starts with
+// piece gw and then takes the next unclaimed piece (one atomic per piece), so
+// a slow piece (measured: a few CTAs of a static partition finish 2-5x after
+// the median on C2 push levels) no longer holds the whole grid at the barrier.
+template <class Front, class Op>
+__device__ __forceinline__ void expand_lb(const Front &fr, const int32_t *__restrict__ C, int64_t gw,
+                                          int64_t nw, Op &op, unsigned long long *work = nullptr,
+                                          int kChunks = 4) {
+    const int64_t F = fr.F, E = fr.E;
+    if (E <= 0 || F <= 0) return;
+    const int64_t D = F + E;
+    if (work == nullptr || D < nw * 256) {
+        const int64_t d0 = (D * gw) / nw;  // D < 2^40, nw < 2^20: no overflow
+        const int64_t d1 = (D * (gw + 1)) / nw;
+        if (d0 < d1) expand_lb_range(fr, C, d0, d1, op);
+        return;
+    }
+    const int64_t P0 = nw * kChunks;
+    int64_t K = (D + P0 - 1) / P0;
+    if (K < kMinChunk) {                   // two searches per piece: keep pieces long,
+        const int64_t Kw = (D + nw - 1) / nw;  // but never fewer pieces than warps
+        K = Kw < kMinChunk ? Kw : kMinChunk;
+    }
+    const int64_t P = (D + K - 1) / K;
+    int64_t c = gw;
+    while (c < P) {
+        const int64_t d0 = c * K;
+        const int64_t d1 = (d0 + K < D) ? d0 + K : D;
+        if (d0 < d1) expand_lb_range(fr, C, d0, d1, op);
+        unsigned long long t = 0;
+        if (lane_id() == 0) t = atomicAdd(work, 1ull);
+        c = nw + (int64_t)__shfl_sync(0xffffffffu, t, 0);
     }
 }
 

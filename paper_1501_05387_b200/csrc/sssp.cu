@@ -150,6 +150,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             a.qo[0][0] = 0;
             a.qr[0][0] = a.R[a.src];
             a.ctl->slot[0].qpack = ((unsigned long long)d << a.S) | 1ull;
+            a.ctl->slot[0].dmax = (unsigned long long)d;
         }
     }
     grid.sync();
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             s->ctl[1] = ld_volatile(&a.ctl->far_count[fp]);
             s->ctl[2] = ld_volatile(&cur.ndisc);
             s->ctl[3] = ld_volatile(&a.ctl->overflow);
+            s->ctl[5] = ld_volatile(&cur.dmax);
             s->bsum[0] = 0;
         }
         __syncthreads();
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         if (tid == 0) {
             Slot &rst = a.ctl->slot[(k + 2) & 3];
             rst.qpack = 0; rst.ndisc = 0; rst.fpack = 0; rst.work = 0; rst.minfar = ~0ull;
-            rst.insp = 0;
+            rst.insp = 0; rst.dmax = 0;
             if (k < kMaxStatRecords) {
                 gr_level_stats &st = a.stats[k];
                 st.level = k; st.direction = f > 0 ? 3 : 4; st.frontier = f > 0 ? f : fc;
@@ -207,6 +209,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         nearq.qo = a.qo[(k + 1) & 1];
         nearq.qr = a.qr[(k + 1) & 1];
         nearq.counter = &nxt.qpack;
+        nearq.dmax = &nxt.dmax;
 
         if (f > 0) {
             // ---- near iteration: Advance(UpdateLabel, SetPred) + Filter ----
@@ -216,13 +219,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.qr[k & 1], f, mf};
             // same auto rule as BFS (reading A-4): short lists -> thread/warp/CTA
-            if (mf <= 16 * f)
+            if (mf <= 16 * f && (int64_t)s->ctl[5] <= kTwcMaxDeg)  // no long list (see bfs.cu)
                 expand_twc(fr, a.C, op, &s->win);
             else
 #if GR_SSSP_PIPE
                 expand_pipe<kSsspStages, true>(fr, a.C, a.W, gw, nw, op, &s->pipe[wib]);
 #else
-                expand_lb(fr, a.C, gw, nw, op);
+                expand_lb(fr, a.C, gw, nw, op, &a.ctl->slot[k & 3].work, 4);
 #endif
             nearq.finish();
             farq.finish();
@@ -292,7 +295,10 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             fp ^= 1;
         }
     }
-    if (tid == 0) a.ctl->levels = (unsigned long long)k;
+    if (tid == 0) {
+        a.ctl->levels = (unsigned long long)k;
+        if (a.ctl->overflow) a.ctl->sticky = 1ull;
+    }
 }
 
 __global__ void unpack_kernel(const unsigned long long *dp, int64_t n, uint32_t *dist, int32_t *pred) {

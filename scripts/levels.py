@@ -12,6 +12,7 @@ ap.add_argument("--directions", default="auto,push")
 ap.add_argument("--nsrc", type=int, default=2)
 ap.add_argument("--delta", type=int, default=0)
 ap.add_argument("--maxrows", type=int, default=40)
+ap.add_argument("--idempotent", type=int, default=0)
 a = ap.parse_args()
 torch.cuda.set_device(0)
 g = gg.make_config(a.config, device="cuda", weights=(a.prim == "sssp") or None)
@@ -45,7 +46,7 @@ for s in SRCS:
     for d in a.directions.split(","):
         for rep in range(3):
             if a.prim == "bfs":
-                G.bfs(s, direction=d)
+                G.bfs(s, direction=d, idempotent=bool(a.idempotent))
             else:
                 G.sssp(s, delta=a.delta)
         torch.cuda.synchronize()

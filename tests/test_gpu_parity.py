@@ -252,3 +252,34 @@ def test_strategies_forced(gr, strategy):
         srcs = gg.sources(g, 2)
         _check_bfs(gr, G, g, srcs, dirs=["push", "auto"], strategy=strategy)
         _check_bfs(gr, G, g, srcs[:1], dirs=["push"], strategy=strategy, idempotent=True)
+
+
+def test_async_runs_match_oracle(gr):
+    """gr_bfs_async / gr_sssp_async enqueue only; after gr_graph_sync the
+    outputs of back-to-back runs equal the oracle's (include/gr.h)."""
+    g = gg.assign_weights(gg.rmat(14, 16, seed=7), seed=8)
+    R, C, W = g.numpy()
+    G = _dev(g, gr)
+    srcs = gg.sources(g, 3)
+    outs = []
+    for s in srcs:  # distinct output buffers, no host sync in between
+        d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        p = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        G.bfs(s, d, p, direction="auto", asynchronous=True)
+        outs.append((s, d, p))
+    dist = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    G.sssp(srcs[0], dist, None, want_pred=False, asynchronous=True)
+    G.sync()
+    for s, d, p in outs:
+        ref, _ = oracle.bfs(R, C, s)
+        got = d.cpu().numpy()
+        assert np.array_equal(got, ref)
+        assert oracle.check_bfs(R, C, s, got, p.cpu().numpy()) == []
+    ref, _ = oracle.sssp(R, C, W, srcs[0])
+    assert np.array_equal(gr.dist_to_u32(dist), ref)
+    # host outputs are refused by the asynchronous entry points
+    host = torch.empty(g.n, dtype=torch.int32)
+    with pytest.raises(gr.GrError):
+        G.bfs(srcs[0], host, None, want_pred=False, asynchronous=True)
+    G.sync()  # nothing pending: OK
+    G.close()
