@@ -157,6 +157,21 @@ def algorithmic_bytes(stats, n, prim):
     return B
 
 
+def load_traffic(workload):
+    """DRAM bytes per launch of the dominant kernel for this workload, from the
+    committed `ncu --set full` capture summary (profiles/ncu_traffic.json:
+    dram__bytes_read.sum + dram__bytes_write.sum of one launch), or None."""
+    p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            rec = json.load(f).get(workload)
+    except (OSError, ValueError):
+        return None, None
+    if not rec:
+        return None, None
+    return rec.get("bytes_per_launch"), rec.get("source")
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -392,11 +407,15 @@ def main():
                 "model": "SURVEY 8(d) algorithmic bytes from per-level run stats (push 12f+4m_f+12d; "
                          "pull n/4+8u+4e_insp+8d; +8n init); one launch per traversal"}
 
+    workload = "%s %s direction=%s" % (args.config, args.prim, args.direction)
+    roofline["traffic"], tsrc = load_traffic(workload)
+    if tsrc:
+        roofline["traffic_source"] = tsrc
     out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": tot_ms_all / args.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None,
            "dtype": "int32" if args.prim == "bfs" else "u32", "data": "synthetic",
-           "config": {"workload": "%s %s direction=%s" % (args.config, args.prim, args.direction),
+           "config": {"workload": workload,
                       "graph": CONFIG_DESC[args.config], "n": n, "m": m,
                       "sources": "%d seeded sources with degree>=1 per rank (S:519)" % args.steps,
                       "l2": "flushed (256 MiB write) between timed steps",
@@ -410,6 +429,11 @@ def main():
     # ---- end to end through the C ABI with host buffers (rank 0 measures; all ranks run)
     pin_d = torch.empty(n, dtype=torch.int32, pin_memory=True)
     pin_p = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    for s in warm_srcs:  # untimed: the first host-output call allocates the staging buffers
+        if args.prim == "bfs":
+            G.bfs(s, pin_d, pin_p, direction=args.direction)
+        else:
+            G.sssp(s, pin_d, pin_p, delta=args.delta)
     e2e_edges, e2e_s = 0, 0.0
     for s in my_srcs:
         torch.cuda.synchronize()

@@ -54,8 +54,12 @@ enum {
                                R[0]=0, R non-decreasing, R[n]=m, 0<=C[e]<n.       */
     GR_KEEP_ORDER = 1u << 3 /* keep the caller's neighbour order. By default every
                                in-list is reordered by neighbour degree (descending)
-                               so pull steps exit early sooner; results (depth,
-                               dist) are unaffected, the parent picked may differ. */
+                               so pull steps exit early sooner; for a GR_SYMMETRIC
+                               graph that reordered copy is separate (4m bytes more)
+                               and the out-lists keep the caller's order (ascending
+                               ids make a warp's culling probes share bitmap lines).
+                               Results (depth, dist) are unaffected, the parent
+                               picked may differ. */
 };
 
 /*

@@ -77,6 +77,7 @@ struct BfsArgs {
     int64_t snap_min_edges;    // push steps with at least this many frontier edges use it
     int32_t lb_chunks;         // dynamic merge-path pieces per warp (0: static partition)
     int32_t claim_cas;         // push claim: CAS on depth[] (1) or atomicOr on the bitmap (0)
+    int64_t probe_skip_pct;    // push steps skip the culling probe while m_u >= this % of m
 };
 
 template <int kNW>
@@ -794,7 +795,11 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
         if (dir == 1) {
             BfsPushOp op{a.visited, st.fbn_clean ? fb_n : nullptr, a.depth, a.pred, a.R, L + 1,
                          a.idempotent, &app, 0ull, pol_keep,
-                         mf < (1 << 16) ? 0 : (snap || st.m_u * 4 >= a.m ? 1 : 2), a.claim_cas, sbm,
+                         // probe: none for small steps and when most edges still lead to
+                         // unvisited vertices (the claim's old bit answers anyway: one random
+                         // line per edge less); L2 while many do; L1 late (mostly visited)
+                         (mf < (1 << 16) || st.m_u * 100 >= a.m * a.probe_skip_pct) ? 0
+                             : (snap || st.m_u * 4 >= a.m ? 1 : 2), a.claim_cas, sbm,
                          snap ? sbits : 0};
             GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.qr[L & 1], f, mf};
             // auto (reading A-4, measured on B200): node-granular thread/warp/CTA
@@ -906,6 +911,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.small_e = env_int("GR_SMALL_E", kSmallE);
     a.lb_chunks = (int32_t)env_int("GR_LB_CHUNKS", 4);
     a.claim_cas = (int32_t)env_int("GR_CLAIM_CAS", 0);
+    a.probe_skip_pct = env_int("GR_PROBE_SKIP_PCT", 75);
     if (a.small_f > kSmallF) a.small_f = kSmallF;
 
     // Kernel variant: graphs whose bitmap no

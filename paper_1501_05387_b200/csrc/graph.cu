@@ -278,6 +278,14 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
         cudaFree(cnt);
     }
     if (!(flags & GR_KEEP_ORDER) && ncols == n && m > 0 && m < (1ll << 31)) {
+        // Symmetric graph: the pull lists get their own copy (Ct != C), so the
+        // push lists keep the caller's order -- usually ascending neighbour id,
+        // which makes the 32 culling probes of one warp into a long list share
+        // a few bitmap lines (a hub's sorted neighbours are dense in id space).
+        if (g->Ct == g->C && env_int("GR_SPLIT_ORDER", 1)) {
+            TRY(dev_alloc(g, (void **)&g->Ct, m * sizeof(int32_t)));
+            TRYC(cudaMemcpyAsync(g->Ct, g->C, m * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+        }
         // Order every in-list (the lists a pull step scans) by the out-degree of
         // the neighbour, descending: the early exit of the bottom-up sweep finds
         // a frontier parent sooner (measured: C3 -20%, C5 -19% per BFS). Any

@@ -1,38 +1,53 @@
 #!/bin/bash
-# One GPU session: bench lines, full-size parity, ncu launch list + full capture.
-# Usage (under gpurun): bash scripts/gpu_measure.sh <tag> [what...]
-# what: bench, configs, launches, ncu, sssp   (default: all)
+# One GPU session: bench lines for every config, ncu launch list and full
+# captures of the top kernel, summaries. Usage (under gpurun):
+#   bash scripts/gpu_measure.sh <tag> [what...]
+# what: bench, configs, launches, ncu   (default: bench launches ncu)
 set -u
 TAG=${1:-r01}; shift || true
-WHAT=${*:-"bench configs launches ncu sssp"}
+WHAT=${*:-"bench launches ncu"}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 nvidia-smi -q -d CLOCK > $OUT/clocks_start.txt 2>&1
+b() {  # name, bench args...
+  local name=$1; shift
+  timeout 900 python bench.py "$@" > $OUT/bench_$name.json 2> $OUT/bench_$name.err; echo "bench $name rc=$?"
+}
 for w in $WHAT; do
 case $w in
 bench)
-  timeout 900 python bench.py > $OUT/bench_c2_auto.json 2> $OUT/bench_c2_auto.err; echo "bench rc=$?"
-  timeout 900 python bench.py --direction push --no-extras > $OUT/bench_c2_push.json 2> $OUT/bench_c2_push.err; echo "bench push rc=$?"
-  ;;
-sssp)
-  timeout 900 python bench.py --config c3_orkut --prim sssp --steps 4 --no-extras > $OUT/bench_c3_sssp.json 2> $OUT/bench_c3_sssp.err; echo "bench c3 sssp rc=$?"
-  timeout 900 python bench.py --config c3_orkut --prim bfs --steps 8 --no-extras > $OUT/bench_c3_bfs.json 2> $OUT/bench_c3_bfs.err; echo "bench c3 bfs rc=$?"
-  timeout 900 python bench.py --config c4_road --prim bfs --steps 4 --no-extras > $OUT/bench_c4_bfs.json 2> $OUT/bench_c4_bfs.err; echo "bench c4 bfs rc=$?"
-  timeout 900 python bench.py --config c4_road --prim sssp --steps 2 --no-extras > $OUT/bench_c4_sssp.json 2> $OUT/bench_c4_sssp.err; echo "bench c4 sssp rc=$?"
+  b c2_auto
+  b c2_push --direction push --no-extras
+  b c1 --config c1_rmat16 --no-extras
+  b c3_bfs --config c3_orkut --prim bfs --no-extras
+  b c3_sssp --config c3_orkut --prim sssp --steps 4 --no-extras
+  b c4_bfs --config c4_road --prim bfs --steps 4 --no-extras
+  b c4_sssp --config c4_road --prim sssp --steps 2 --no-extras
+  b c5 --config c5_kron25 --steps 8 --no-extras --cpu-sample-s 10
   ;;
 configs)
   timeout 1500 python -m pytest tests -m "gpu and slow" -x -q > $OUT/configs_tests.log 2>&1; echo "configs rc=$?"; tail -5 $OUT/configs_tests.log
   ;;
 launches)
-  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-     python bench.py --steps 4 --warmup 1 --no-cpu-baseline --no-extras > $OUT/launches_bench.json 2>&1; echo "launches rc=$?"
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c2_auto.csv \
+     python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-extras > $OUT/launches_bench.json 2>&1; echo "launches rc=$?"
   ;;
 ncu)
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:bfs_kernel -s 2 -c 1 \
-     -o $OUT/prof_bfs_push python bench.py --steps 2 --warmup 1 --direction push --no-cpu-baseline --no-extras > $OUT/ncu_push.log 2>&1; echo "ncu push rc=$?"
-  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:bfs_kernel -s 2 -c 1 \
-     -o $OUT/prof_bfs_auto python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-extras > $OUT/ncu_auto.log 2>&1; echo "ncu auto rc=$?"
+  for d in auto push; do
+    timeout 1200 ncu --set full --clock-control none --import-source on -k regex:bfs_kernel -s 3 -c 1 \
+       -o $OUT/prof_c2_$d python bench.py --steps 2 --warmup 3 --direction $d --no-cpu-baseline --no-extras \
+       > $OUT/ncu_c2_$d.log 2>&1; echo "ncu c2 $d rc=$?"
+    python scripts/ncu_summary.py $OUT/prof_c2_$d.ncu-rep $OUT/ncu_c2_${d}_bfs_kernel.txt
+  done
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:sssp_kernel -s 1 -c 1 \
+     -o $OUT/prof_c3_sssp python bench.py --config c3_orkut --prim sssp --steps 1 --warmup 3 --no-cpu-baseline \
+     --no-extras > $OUT/ncu_c3_sssp.log 2>&1; echo "ncu c3 sssp rc=$?"
+  python scripts/ncu_summary.py $OUT/prof_c3_sssp.ncu-rep $OUT/ncu_c3_sssp_kernel.txt
   ;;
 esac
 done
-for f in $OUT/*.json; do echo "== $f"; head -c 1500 $f; echo; done
+for f in $OUT/bench_*.json; do echo "== $f"; python -c "
+import json,sys
+d=json.load(open('$f')); r=d['roofline']
+print(d['config']['workload'], 'value %.2f %s' % (d['value'], d['unit']), 'ms %.4f' % d['ms_per_step'],
+      'frac %.4f' % r['frac'], 'e2e %.2f' % d['e2e']['value'], 'cpu', d.get('cpu_baseline', {}).get('value'))" 2>&1 | tail -1; done

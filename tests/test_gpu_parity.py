@@ -283,3 +283,22 @@ def test_async_runs_match_oracle(gr):
         G.bfs(srcs[0], host, None, want_pred=False, asynchronous=True)
     G.sync()  # nothing pending: OK
     G.close()
+
+
+@pytest.mark.parametrize("env", [{}, {"GR_LB_CHUNKS": "16"}, {"GR_LB_CHUNKS": "0"},
+                                 {"GR_PROBE_SKIP_PCT": "0"}, {"GR_SPLIT_ORDER": "0"},
+                                 {"GR_CLAIM_CAS": "1"}])
+def test_mid_size_variants(gr, env, monkeypatch):
+    """Sizes where the grid-level machinery engages (dynamic merge-path pieces
+    need >= 256 items per warp; long in-lists reach the warp scan of the pull
+    step; pull -> push transitions rebuild the queue from the bitmap), under
+    each tuning knob's alternative setting."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    graphs = [gg.kronecker(17, 16, seed=11), gg.make_config("c3_orkut", shrink=3),
+              gg.directed_random(200_000, 2_000_000, seed=12)]
+    for g in graphs:
+        G = _dev(g, gr)
+        _check_bfs(gr, G, g, gg.sources(g, 2), dirs=["push", "auto", "pull"])
+        _check_bfs(gr, G, g, gg.sources(g, 1), dirs=["auto"], idempotent=True)
+        G.close()
