@@ -71,11 +71,11 @@ def parse():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--partitioned", action="store_true",
-                    help="1D-partitioned BFS over all ranks (NCCL exchange per level); "
-                         "default graph c5_kron25")
+                    help="1D-partitioned BFS / SSSP over all ranks (NCCL exchange per step); "
+                         "default graph c5_kron25 (BFS) / c3_orkut (SSSP)")
     a = ap.parse_args()
     if a.partitioned and a.config == "c2_kron21" and "--config" not in sys.argv:
-        a.config = "c5_kron25"
+        a.config = "c3_orkut" if a.prim == "sssp" else "c5_kron25"
     return a
 
 
@@ -241,20 +241,32 @@ def run_partitioned(args, rank, world, dev):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
-    g = gg.make_config(args.config, device=dev)
+    sssp = args.prim == "sssp"
+    g = gg.make_config(args.config, device=dev, weights=True if sssp else None)
     srcs = gg.sources(g, args.warmup + args.steps)
     v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, world, rank)
+    Wl = grd.partition_weights(g.R, g.W, world, rank) if sssp else None
     deg_local = (Rl[1:] - Rl[:-1])
     n, m = g.n, g.m
-    part = grd.GpuPartition(Rl, Cl, n, world, rank, device=dev.index)
+    delta = args.delta
+    if sssp and delta == 0:  # the single-GPU auto rule (reading A-10, abi.cu)
+        mw = int(g.W.max())
+        delta = max(1, (mw + 10) // 21) if m / n >= 8.0 else mw * 32
+    part = grd.GpuPartition(Rl, Cl, n, world, rank, device=dev.index, W_local=Wl)
     del g
     torch.cuda.empty_cache()
     ex = grd.TorchDistExchange()
     depth = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
     pred = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def run(s):
+        if sssp:
+            return grd.sssp_partitioned(part, ex, s, depth, pred, delta=delta)
+        return grd.bfs_partitioned(part, ex, s, depth, pred)
+
     for s in srcs[: args.warmup]:
-        grd.bfs_partitioned(part, ex, s, depth, pred)
+        run(s)
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = gr.gr_kernel_launch_count()
@@ -265,13 +277,14 @@ def run_partitioned(args, rank, world, dev):
             dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            levels.append(grd.bfs_partitioned(part, ex, s, depth, pred))
+            levels.append(run(s))
             e1.record()
             torch.cuda.synchronize()
             t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot_ms += float(t[0])
-            r = torch.tensor([int(deg_local[depth >= 0].sum())], dtype=torch.int64, device=dev)
+            reached = (depth != -1) if sssp else (depth >= 0)  # uint32 max reads as -1
+            r = torch.tensor([int(deg_local[reached].sum())], dtype=torch.int64, device=dev)
             dist.all_reduce(r)
             edges += int(r[0])
     launches = gr.gr_kernel_launch_count() - launches0
@@ -280,10 +293,14 @@ def run_partitioned(args, rank, world, dev):
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-               "config": {"workload": "%s bfs 1D-partitioned direction-optimizing: push levels "
-                                      "NCCL all-to-all of (vertex,parent), pull levels NCCL all-gather "
-                                      "of the frontier bitmap" % args.config,
+               "scaling": "strong", "vs_baseline": None, "dtype": "u32" if sssp else "int32",
+               "data": "synthetic",
+               "config": {"workload": ("%s sssp 1D-partitioned near/far delta-stepping (delta %d): NCCL "
+                                       "all-to-all of (vertex,dist,parent) triples per near iteration, "
+                                       "all-reduced far minimum per re-split" % (args.config, delta)) if sssp else
+                                      ("%s bfs 1D-partitioned direction-optimizing: push levels "
+                                       "NCCL all-to-all of (vertex,parent), pull levels NCCL all-gather "
+                                       "of the frontier bitmap" % args.config),
                           "graph": CONFIG_DESC[args.config], "n": n, "m": m,
                           "parallelism": "1D vertex partition over %d rank(s)" % world,
                           "l2": "flushed (256 MiB write) between timed steps"},
@@ -426,29 +443,6 @@ def main():
         out["paper_context"] = PAPER_CONTEXT.get((args.config, args.prim))
         out["levels_per_step"] = statistics.mean(r["num_levels"] for r in recs)
 
-    # ---- end to end through the C ABI with host buffers (rank 0 measures; all ranks run)
-    pin_d = torch.empty(n, dtype=torch.int32, pin_memory=True)
-    pin_p = torch.empty(n, dtype=torch.int32, pin_memory=True)
-    for s in warm_srcs:  # untimed: the first host-output call allocates the staging buffers
-        if args.prim == "bfs":
-            G.bfs(s, pin_d, pin_p, direction=args.direction)
-        else:
-            G.sssp(s, pin_d, pin_p, delta=args.delta)
-    e2e_edges, e2e_s = 0, 0.0
-    for s in my_srcs:
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        if args.prim == "bfs":
-            G.bfs(s, pin_d, pin_p, direction=args.direction)
-        else:
-            G.sssp(s, pin_d, pin_p, delta=args.delta)
-        e2e_s += time.perf_counter() - t0
-        e2e_edges += reached(pin_d.to(dev))
-    out["e2e"] = {"value": e2e_edges / e2e_s / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 0,
-                  "d2h_bytes_per_step": 8 * n,
-                  "what": "gr_bfs/gr_sssp through the C ABI writing host (pinned) depth+pred; "
-                          "host wall clock per call; graph resident (created once, P:1089-1090)"}
-
     if rank == 0 and not args.no_extras and args.prim == "bfs" and args.direction == "auto":
         # the push-only roofline row of the north star (same sources)
         pe, pms, precs = timed(my_srcs, "push")
@@ -457,6 +451,37 @@ def main():
         out["push_only"] = {"value": pe / (sum(pms) * 1e-3) / 1e9, "unit": "GTEPS",
                             "ms_per_step": sum(pms) / len(pms), "achieved_gbs": pach,
                             "frac": pach / peak}
+        # north-star reading of the bar: "bytes touched per traversed edge x
+        # TEPS / peak" with the push-only byte model (SURVEY 8(d) M-1 F_edge,
+        # "push-equivalent"): credits the edges direction optimisation skips
+        roofline["push_equivalent"] = {
+            "achieved": sum(pb) / (tot_ms * 1e-3) / 1e9, "frac": sum(pb) / (tot_ms * 1e-3) / 1e9 / peak,
+            "what": "F_edge (SURVEY 8(d) M-1): push-only model bytes of the same sources / push-pull time / peak"}
+
+    # ---- end to end through the C ABI with host buffers (rank 0 measures; all ranks run)
+    pin_d = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    pin_p = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    for s in warm_srcs:  # untimed: the first host-output call allocates the staging buffers
+        if args.prim == "bfs":
+            G.bfs(s, pin_d, pin_p, direction=args.direction)
+        else:
+            G.sssp(s, pin_d, pin_p, delta=args.delta)
+    e2e_edges, e2e_s, per_call = 0, 0.0, []
+    for s in my_srcs:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if args.prim == "bfs":
+            G.bfs(s, pin_d, pin_p, direction=args.direction)
+        else:
+            G.sssp(s, pin_d, pin_p, delta=args.delta)
+        per_call.append(time.perf_counter() - t0)
+        e2e_s += per_call[-1]
+        e2e_edges += reached(pin_d.to(dev))
+    out["e2e"] = {"value": e2e_edges / e2e_s / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                  "d2h_bytes_per_step": 8 * n,
+                  "what": "gr_bfs/gr_sssp through the C ABI writing host (pinned) depth+pred; "
+                          "host wall clock per call; graph resident (created once, P:1089-1090)",
+                  "per_call_ms": [round(x * 1e3, 3) for x in per_call]}
 
     if rank == 0 and not args.no_cpu_baseline:
         import oracle

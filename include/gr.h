@@ -136,7 +136,9 @@ typedef struct {
                             "unvisited < frontier" (A-3)                */
     double alpha, beta;  /* Beamer parameters; 0 = 14, 24                          */
     int64_t lb_threshold;/* frontier size at which auto strategy switches from
-                            node-granular to edge-granular balancing; 0 = default   */
+                            node-granular to edge-granular balancing; 0 = default
+                            65536 (swept on B200, scripts/lb_sweep.py; auto also
+                            needs short lists: m_f <= 16 f, max degree <= 4096) */
 } gr_bfs_opts;
 
 gr_status gr_bfs(gr_graph *g, int32_t src, int32_t *depth_out, int32_t *pred_out,
@@ -283,6 +285,64 @@ gr_status gr_part_bfs_frontier(gr_graph *g, int32_t level, int64_t *f, int64_t *
  * block is a multiple of 32 (block = 32*ceil(n/(32*nparts))). */
 gr_status gr_part_bfs_shard(gr_graph *g, int32_t level, uint32_t *shard);
 gr_status gr_part_bfs_pull(gr_graph *g, int32_t level, const uint32_t *global_frontier);
+
+/* ===========================================================================
+ * Multi-GPU SSSP over the same 1D partition. The paper's
+ * near/far delta-stepping (Alg. 1; "an additional
+ * filter pass between two iterations") runs per partition; the
+ * caller drives the steps, exchanges the triples and reduces the counters
+ * (paper_1501_05387_b200/dist.py: sssp_partitioned). Per step k:
+ *   near queue non-empty (globally): it += 1;
+ *     gr_part_sssp_relax(k, it, fp, thr)  local relax (owned targets: packed
+ *         atomicMin dist|pred (A-9), iteration+slice stamp (A-7), near/far
+ *         append); remote targets: this rank's best-shipped value per vertex
+ *         is lowered by atomicMin and each improved vertex enters the bucket
+ *         of its owner once per step, then its final best value is packed as
+ *         a (vertex, dist, parent) int32 triple;
+ *     (exchange) all-to-all of the bucket sizes, then of the triples;
+ *     gr_part_sssp_absorb(k, it, fp, thr, recv, nrecv)  owner relaxes them;
+ *   near queue empty everywhere:
+ *     gr_part_sssp_far_min(k, fp, thr)  -> local min far distance >= thr
+ *         (UINT64_MAX if none); the caller all-reduces MIN; if none: done;
+ *     thr' = (floor(min / delta) + 1) * delta; it += 1;
+ *     gr_part_sssp_resplit(k, it, fp, thr, thr')  far pile fp -> near queue
+ *         of step k+1 and far pile fp^1, stale entries (dist < thr) dropped
+ *         (A-11); then fp ^= 1;
+ *   k += 1; gr_part_sssp_counts(k, fp) gives the local near size (summed by
+ *   the caller) and far size.
+ * Starts: thr = delta (>= 1), it = 0, fp = 0, k = 0. Ends: gr_part_sssp_end
+ * writes dist (UINT32_MAX unreached) and pred (GLOBAL ids, -1 unreached,
+ * pred[src] = src) of the owned block into the buffers given to begin.
+ * Errors: GR_ERR_NO_WEIGHTS (partition created without weights),
+ * GR_ERR_OVERFLOW (max_w * (n_global-1) may overflow uint32, or a queue
+ * outgrew its capacity, reported by gr_part_sssp_counts),
+ * GR_ERR_OUT_OF_RANGE (src), GR_ERR_INVALID_ARGUMENT (host outputs, bad
+ * step / iteration / pile indices, thr' <= thr).
+ * =========================================================================== */
+
+/* gr_graph_create_part with edge weights uint32[m_local] (host or device,
+ * copied), aligned with col_indices (weights 1..64). */
+gr_status gr_graph_create_part_w(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin,
+                                 int64_t v_end, int64_t m_local, const int64_t *row_offsets,
+                                 const int32_t *col_indices, const uint32_t *weights, uint32_t flags,
+                                 int device, void *cuda_stream, gr_graph **out);
+/* dist_out uint32[v_end - v_begin], pred_out int32[...] or NULL: DEVICE memory. */
+gr_status gr_part_sssp_begin(gr_graph *g, int64_t src, uint32_t *dist_out, int32_t *pred_out);
+/* send_triples int32[3 * nparts * block] (bucket of peer q at 3*q*block),
+ * send_counts int64[nparts] (triples per bucket after relax),
+ * recv_triples int32[3 * nparts * block] (where the caller gathers incoming
+ * triples). Valid after gr_part_sssp_begin, for the graph's lifetime. */
+gr_status gr_part_sssp_buffers(gr_graph *g, int32_t **send_triples, int64_t **send_counts,
+                               int32_t **recv_triples, int64_t *block);
+gr_status gr_part_sssp_relax(gr_graph *g, int32_t step, int32_t it, int32_t fp, uint64_t thr);
+gr_status gr_part_sssp_absorb(gr_graph *g, int32_t step, int32_t it, int32_t fp, uint64_t thr,
+                              const int32_t *recv_triples, int64_t nrecv);
+gr_status gr_part_sssp_counts(gr_graph *g, int32_t step, int32_t fp, int64_t *near_count,
+                              int64_t *far_count);
+gr_status gr_part_sssp_far_min(gr_graph *g, int32_t step, int32_t fp, uint64_t thr, uint64_t *min_out);
+gr_status gr_part_sssp_resplit(gr_graph *g, int32_t step, int32_t it, int32_t fp, uint64_t thr_old,
+                               uint64_t thr);
+gr_status gr_part_sssp_end(gr_graph *g);
 
 #ifdef __cplusplus
 }

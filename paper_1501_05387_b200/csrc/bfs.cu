@@ -902,7 +902,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.switch_rule = o.switch_rule;
     a.idempotent = o.idempotent;
     a.strategy = o.strategy;
-    a.lb_threshold = o.lb_threshold > 0 ? o.lb_threshold : env_int("GR_LB_THRESHOLD", 1ll << 40);
+    a.lb_threshold = o.lb_threshold > 0 ? o.lb_threshold : env_int("GR_LB_THRESHOLD", 65536);
     a.alpha = o.alpha > 0 ? o.alpha : 14.0;
     a.beta = o.beta > 0 ? o.beta : 24.0;
     a.nonisolated = g->nonisolated;

@@ -131,6 +131,13 @@ struct Graph {
     long long *send_counts = nullptr;  // [nparts]
     int32_t *recv_pairs = nullptr;     // [2 * n_global]
     int32_t *part_depth = nullptr, *part_pred = nullptr;
+    // partitioned SSSP (partition_sssp.cu)
+    unsigned long long *ps_best = nullptr;  // [n_global] best (dist<<32|pred) shipped per remote vertex
+    int32_t *ps_sstamp = nullptr;           // [n_global] step of the last shipment (one per step)
+    int32_t *ps_send = nullptr;             // [3 * nparts * block] (vertex, dist, parent) triples
+    int32_t *ps_recv = nullptr;             // [3 * nparts * block]
+    uint32_t *ps_dist = nullptr;            // caller's outputs (gr_part_sssp_begin)
+    int32_t *ps_pred = nullptr;
 };
 
 gr_status dev_alloc(Graph *g, void **p, size_t bytes);

@@ -285,9 +285,10 @@ using namespace gr;
 
 extern "C" {
 
-gr_status gr_graph_create_part(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin, int64_t v_end,
-                               int64_t m_local, const int64_t *row_offsets, const int32_t *col_indices,
-                               uint32_t flags, int device, void *cuda_stream, gr_graph **out) {
+static gr_status create_part(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin, int64_t v_end,
+                             int64_t m_local, const int64_t *row_offsets, const int32_t *col_indices,
+                             const uint32_t *weights, uint32_t flags, int device, void *cuda_stream,
+                             gr_graph **out) {
     if (!out || nparts < 1 || rank < 0 || rank >= nparts || n_global < 1) {
         set_error("invalid partition arguments (nparts=%d rank=%d n_global=%lld)", nparts, rank, (long long)n_global);
         return GR_ERR_INVALID_ARGUMENT;
@@ -300,7 +301,7 @@ gr_status gr_graph_create_part(int64_t n_global, int32_t nparts, int32_t rank, i
         return GR_ERR_INVALID_ARGUMENT;
     }
     Graph *g = nullptr;
-    gr_status st = graph_create(v_end - v_begin, m_local, row_offsets, col_indices, nullptr, flags, device,
+    gr_status st = graph_create(v_end - v_begin, m_local, row_offsets, col_indices, weights, flags, device,
                                 cuda_stream, &g, n_global);
     if (st != GR_OK) return st;
     g->part = true;
@@ -316,6 +317,24 @@ gr_status gr_graph_create_part(int64_t n_global, int32_t nparts, int32_t rank, i
     }
     *out = (gr_graph *)g;
     return GR_OK;
+}
+
+gr_status gr_graph_create_part(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin, int64_t v_end,
+                               int64_t m_local, const int64_t *row_offsets, const int32_t *col_indices,
+                               uint32_t flags, int device, void *cuda_stream, gr_graph **out) {
+    return create_part(n_global, nparts, rank, v_begin, v_end, m_local, row_offsets, col_indices, nullptr, flags,
+                       device, cuda_stream, out);
+}
+
+gr_status gr_graph_create_part_w(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin, int64_t v_end,
+                                 int64_t m_local, const int64_t *row_offsets, const int32_t *col_indices,
+                                 const uint32_t *weights, uint32_t flags, int device, void *cuda_stream,
+                                 gr_graph **out) {
+    if (!weights && m_local > 0) { set_error("weights is NULL"); return GR_ERR_NO_WEIGHTS; }
+    gr_status st = create_part(n_global, nparts, rank, v_begin, v_end, m_local, row_offsets, col_indices, weights,
+                               flags, device, cuda_stream, out);
+    if (st == GR_OK) ((Graph *)*out)->has_w = true;  // m_local = 0: no weight is ever read
+    return st;
 }
 
 gr_status gr_part_buffers(gr_graph *h, int32_t **send_pairs, int64_t **send_counts, int32_t **recv_pairs,

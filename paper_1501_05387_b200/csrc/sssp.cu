@@ -30,6 +30,7 @@ struct SsspArgs {
     gr_level_stats *stats;
     int32_t src;
     uint64_t delta;
+    int64_t lb_threshold;     // auto strategy: thread/warp/CTA only below this frontier size (A-4)
     int S;
 };
 
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.qr[k & 1], f, mf};
             // same auto rule as BFS (reading A-4): short lists -> thread/warp/CTA
-            if (mf <= 16 * f && (int64_t)s->ctl[5] <= kTwcMaxDeg)  // no long list (see bfs.cu)
+            if (f < a.lb_threshold && mf <= 16 * f && (int64_t)s->ctl[5] <= kTwcMaxDeg)  // no long list (see bfs.cu)
                 expand_twc(fr, a.C, op, &s->win);
             else
 #if GR_SSSP_PIPE
@@ -323,6 +324,7 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.ctl = g->ctl; a.stats = g->stats_dev;
     a.src = src;
     a.delta = delta;
+    a.lb_threshold = env_int("GR_SSSP_LB_THRESHOLD", 65536);
     a.S = g->pack_shift;
     static int per_sm = 0;
     const size_t smem = sizeof(SsspSmem);

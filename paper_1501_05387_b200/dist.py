@@ -31,6 +31,7 @@ import torch
 from . import GrError, _check, _ptr, load
 
 GR_VALIDATE = 4
+NO_FAR = (1 << 63) - 1   # "no live far entry" (int64 max: all-reducible as int64)
 
 
 def block_size(n: int, nparts: int) -> int:
@@ -52,6 +53,13 @@ def partition_csr(R: torch.Tensor, C: torch.Tensor, nparts: int, rank: int):
     return v0, v1, (R[v0:v1 + 1] - e0).contiguous(), C[e0:e1].contiguous()
 
 
+def partition_weights(R: torch.Tensor, W: torch.Tensor, nparts: int, rank: int):
+    """Weights of the owned block's rows (aligned with partition_csr's C)."""
+    n = R.numel() - 1
+    v0, v1 = owned_range(n, nparts, rank)
+    return W[int(R[v0]):int(R[v1])].contiguous()
+
+
 class _CudaArray:
     """Wraps a raw device pointer for torch.as_tensor (no copy)."""
 
@@ -64,7 +72,7 @@ class GpuPartition:
     """The partition of this rank on one GPU (C ABI gr_graph_create_part)."""
 
     def __init__(self, R_local, C_local, n_global: int, nparts: int, rank: int, device: int = None,
-                 stream=None, validate: bool = True, symmetric: bool = True):
+                 stream=None, validate: bool = True, symmetric: bool = True, W_local=None):
         self.symmetric = symmetric
         if device is None:
             device = torch.cuda.current_device()
@@ -77,10 +85,19 @@ class GpuPartition:
         h = ctypes.c_void_p()
         rp, rk = _ptr(R_local)
         cp, ck = _ptr(C_local)
-        _check(load().gr_graph_create_part(n_global, nparts, rank, self.v_begin, self.v_end,
-                                           int(C_local.numel()), rp, cp,
-                                           GR_VALIDATE if validate else 0, device,
-                                           ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
+        if W_local is None:
+            _check(load().gr_graph_create_part(n_global, nparts, rank, self.v_begin, self.v_end,
+                                               int(C_local.numel()), rp, cp,
+                                               GR_VALIDATE if validate else 0, device,
+                                               ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
+        else:
+            wp, wk = _ptr(W_local)
+            _check(load().gr_graph_create_part_w(n_global, nparts, rank, self.v_begin, self.v_end,
+                                                 int(C_local.numel()), rp, cp, wp,
+                                                 GR_VALIDATE if validate else 0, device,
+                                                 ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
+        self.weighted = W_local is not None
+        self._ps = None
         self.handle = h
         sp, sc, rv = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
         blk = ctypes.c_int64()
@@ -139,6 +156,45 @@ class GpuPartition:
     def pull(self, level: int, global_bits: torch.Tensor):
         _check(load().gr_part_bfs_pull(self.handle, level, global_bits.data_ptr()))
 
+    # ---- partitioned SSSP (gr_part_sssp_*) -----------------
+    def sssp_begin(self, src: int, dist: torch.Tensor, pred: torch.Tensor = None):
+        """dist: int32 device tensor holding uint32 bits [n_local]; pred int32 or None."""
+        _check(load().gr_part_sssp_begin(self.handle, int(src), dist.data_ptr(),
+                                         pred.data_ptr() if pred is not None else None))
+        if self._ps is None:
+            st, sc, rv = ctypes.c_void_p(), ctypes.c_void_p(), ctypes.c_void_p()
+            blk = ctypes.c_int64()
+            _check(load().gr_part_sssp_buffers(self.handle, ctypes.byref(st), ctypes.byref(sc),
+                                               ctypes.byref(rv), ctypes.byref(blk)))
+            dev = torch.device("cuda", self.device)
+            P, B = self.nparts, blk.value
+            self._ps = (torch.as_tensor(_CudaArray(st.value, 3 * P * B, "<i4", self.device), device=dev),
+                        torch.as_tensor(_CudaArray(rv.value, 3 * P * B, "<i4", self.device), device=dev))
+        self.send_triples, self.recv_triples = self._ps
+
+    def sssp_relax(self, step: int, it: int, fp: int, thr: int):
+        _check(load().gr_part_sssp_relax(self.handle, step, it, fp, thr))
+
+    def sssp_absorb(self, step: int, it: int, fp: int, thr: int, triples: torch.Tensor, nrecv: int):
+        if nrecv:
+            _check(load().gr_part_sssp_absorb(self.handle, step, it, fp, thr, triples.data_ptr(), int(nrecv)))
+
+    def sssp_counts(self, step: int, fp: int):
+        f, fc = ctypes.c_int64(), ctypes.c_int64()
+        _check(load().gr_part_sssp_counts(self.handle, step, fp, ctypes.byref(f), ctypes.byref(fc)))
+        return f.value, fc.value
+
+    def sssp_far_min(self, step: int, fp: int, thr: int) -> int:
+        mn = ctypes.c_uint64()
+        _check(load().gr_part_sssp_far_min(self.handle, step, fp, thr, ctypes.byref(mn)))
+        return mn.value if mn.value != (1 << 64) - 1 else NO_FAR
+
+    def sssp_resplit(self, step: int, it: int, fp: int, thr_old: int, thr: int):
+        _check(load().gr_part_sssp_resplit(self.handle, step, it, fp, thr_old, thr))
+
+    def sssp_end(self):
+        _check(load().gr_part_sssp_end(self.handle))
+
 
 class TorchDistExchange:
     """Exchange over a torch.distributed process group (NCCL or gloo)."""
@@ -162,6 +218,10 @@ class TorchDistExchange:
 
     def allreduce_sum(self, x: torch.Tensor) -> torch.Tensor:
         self.dist.all_reduce(x, group=self.group)
+        return x
+
+    def allreduce_min(self, x: torch.Tensor) -> torch.Tensor:
+        self.dist.all_reduce(x, op=self.dist.ReduceOp.MIN, group=self.group)
         return x
 
     def allgather(self, shard: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
@@ -238,6 +298,60 @@ def bfs_partitioned(part, exchange, src: int, depth: torch.Tensor, pred: torch.T
     return level
 
 
+def next_threshold(mn: int, delta: int) -> int:
+    """Band jump of the far re-split (reading A-11): the threshold
+    moves to the end of the delta-band holding the minimum far distance."""
+    return (mn // delta + 1) * delta
+
+
+def sssp_partitioned(part, exchange, src: int, dist: torch.Tensor, pred: torch.Tensor = None,
+                     delta: int = 1, trace: list = None):
+    """Near/far delta-stepping SSSP (Alg. 1) over the 1D
+    partition of this rank; every rank calls it with the same arguments.
+    Near iterations relax + all-to-all the (vertex, dist, parent) triples +
+    absorb; when the near queues are empty on every rank, the far piles are
+    re-split at the all-reduced minimum (A-11). Returns the number of steps."""
+    if delta < 1:
+        raise ValueError("delta must be >= 1")
+    dev = dist.device
+    part.sssp_begin(src, dist, pred)
+    k, it, fp, thr = 0, 0, 0, int(delta)
+    f = int(exchange.allreduce_sum(torch.tensor([part.sssp_counts(0, fp)[0]], dtype=torch.int64,
+                                                device=dev)).item())
+    while True:
+        if f > 0:
+            it += 1
+            if trace is not None:
+                trace.append(("near", k, it, thr, f))
+            part.sssp_relax(k, it, fp, thr)
+            sc = part.send_counts.clone() if part.send_counts.device == dev else part.send_counts.to(dev)
+            rc = exchange.counts(sc)
+            sc_h, rc_h = sc.tolist(), rc.tolist()
+            B = part.block
+            send_flat = torch.cat([part.send_triples[3 * q * B: 3 * q * B + 3 * int(c)]
+                                   for q, c in enumerate(sc_h)])
+            nrecv = int(sum(rc_h))
+            out = part.recv_triples[: 3 * nrecv]
+            exchange.pairs(send_flat, out, [3 * c for c in sc_h], [3 * c for c in rc_h])
+            part.sssp_absorb(k, it, fp, thr, out, nrecv)
+        else:
+            mn = part.sssp_far_min(k, fp, thr)
+            mn = int(exchange.allreduce_min(torch.tensor([mn], dtype=torch.int64, device=dev)).item())
+            if mn == NO_FAR:
+                break
+            thr_old, thr = thr, next_threshold(mn, int(delta))
+            it += 1
+            if trace is not None:
+                trace.append(("resplit", k, it, thr, mn))
+            part.sssp_resplit(k, it, fp, thr_old, thr)
+            fp ^= 1
+        k += 1
+        f = int(exchange.allreduce_sum(torch.tensor([part.sssp_counts(k, fp)[0]], dtype=torch.int64,
+                                                    device=dev)).item())
+    part.sssp_end()
+    return k
+
+
 class LoopbackGroup:
     """P partitions in ONE process (one GPU): the exchange is a device copy.
     Tests the partition kernels' routing without a second GPU."""
@@ -287,3 +401,38 @@ class LoopbackGroup:
             u -= f
             m_u -= mf
         return level
+
+    def sssp(self, src: int, dists, preds, delta: int = 1):
+        """Partitioned SSSP of all partitions in this process (device-copy exchange)."""
+        P = len(self.parts)
+        for q, pt in enumerate(self.parts):
+            pt.sssp_begin(src, dists[q], preds[q] if preds else None)
+        k, it, fp, thr = 0, 0, 0, int(delta)
+        f = sum(pt.sssp_counts(0, fp)[0] for pt in self.parts)
+        while True:
+            if f > 0:
+                it += 1
+                for pt in self.parts:
+                    pt.sssp_relax(k, it, fp, thr)
+                counts = [pt.send_counts.tolist() for pt in self.parts]
+                for dst in range(P):
+                    pieces = [self.parts[s].send_triples[3 * dst * self.parts[s].block:
+                                                         3 * dst * self.parts[s].block + 3 * counts[s][dst]]
+                              for s in range(P)]
+                    flat = torch.cat(pieces)
+                    self.parts[dst].recv_triples[: flat.numel()].copy_(flat)
+                    self.parts[dst].sssp_absorb(k, it, fp, thr, self.parts[dst].recv_triples, flat.numel() // 3)
+            else:
+                mn = min(pt.sssp_far_min(k, fp, thr) for pt in self.parts)
+                if mn == NO_FAR:
+                    break
+                thr_old, thr = thr, next_threshold(mn, int(delta))
+                it += 1
+                for pt in self.parts:
+                    pt.sssp_resplit(k, it, fp, thr_old, thr)
+                fp ^= 1
+            k += 1
+            f = sum(pt.sssp_counts(k, fp)[0] for pt in self.parts)
+        for pt in self.parts:
+            pt.sssp_end()
+        return k
