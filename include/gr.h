@@ -220,6 +220,24 @@ uint64_t gr_kernel_launch_count(void);
 const char *gr_version(void);
 
 /* ===========================================================================
+ * Betweenness centrality (paper §5.3: Brandes's
+ * formulation, "a forward BFS pass to accumulate sigma values for each node,
+ * and a backward BFS pass to compute centrality values").
+ *   bc_out[v] = sum over s in sources of delta_s(v),
+ *   delta_s(v) = sum over t != s, v of sigma_st(v) / sigma_st
+ * (shortest = fewest edges along CSR out-edges; sigma_st = number of shortest
+ * s->t paths, sigma_st(v) = those through v; delta_s(s) = 0). No halving:
+ * for an undirected (symmetric) graph and sources = all vertices, Brandes's
+ * betweenness (each unordered pair once) is bc_out / 2.
+ * sources: HOST int32[nsrc], each in [0, n) (GR_ERR_OUT_OF_RANGE otherwise).
+ * bc_out: double[n], host or device (overwritten). sigma_out: double[n] or
+ * NULL: sigma_s of the LAST source (host or device). fp64 throughout; path
+ * counts beyond ~1e308 (very high-diameter meshes) overflow to inf.
+ * Synchronous: one host read per BFS level of each source.
+ * =========================================================================== */
+gr_status gr_bc(gr_graph *g, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out);
+
+/* ===========================================================================
  * Multi-GPU: 1D vertex partition (the paper is single-GPU and
  * lists multi-GPU as future work). One process per GPU. Rank q of
  * P owns the contiguous vertex block [q*B, min(n, (q+1)*B)), B = 32*ceil(n/(32P))

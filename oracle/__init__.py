@@ -8,6 +8,7 @@ Contents
 --------
 * bfs(R, C, src)        -> (depth int32[n], pred int32[n])  FIFO-queue BFS (oracle.c)
 * sssp(R, C, W, src)    -> (dist uint32[n], pred int32[n])  binary-heap Dijkstra (oracle.c)
+* bc(R, C, sources)     -> float64[n]  Brandes 2001 Algorithm 1 (oracle.c)
 * check_bfs / check_sssp -- O(m) certificates: they decide
   exactness of depth / dist without any reference output, and validate any
   predecessor array (pred is "any valid parent": parity-unpinned by design,
@@ -51,6 +52,8 @@ def _load():
         lib.oracle_bfs.restype = ctypes.c_int
         lib.oracle_sssp.argtypes = [ctypes.c_int64, p, p, p, ctypes.c_int32, p, p]
         lib.oracle_sssp.restype = ctypes.c_int
+        lib.oracle_bc.argtypes = [ctypes.c_int64, p, p, p, ctypes.c_int64, p]
+        lib.oracle_bc.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -88,6 +91,19 @@ def sssp(R, C, W, src: int, want_pred: bool = True):
     if rc != 0:
         raise ValueError("oracle_sssp failed with code %d" % rc)
     return dist, pred
+
+
+def bc(R, C, sources):
+    """Sum over `sources` of Brandes's dependency delta_s(v) (no halving)."""
+    R = _as(R, np.int64)
+    C = _as(C, np.int32)
+    S = _as(list(sources), np.int32)
+    n = R.size - 1
+    out = np.empty(n, np.float64)
+    rc = _load().oracle_bc(n, _ptr(R), _ptr(C), _ptr(S), int(S.size), _ptr(out))
+    if rc != 0:
+        raise ValueError("oracle_bc failed with code %d" % rc)
+    return out
 
 
 # ---------------------------------------------------------------------------

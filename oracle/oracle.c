@@ -24,6 +24,17 @@
  *                  pred[v] = the vertex whose relaxation last lowered dist[v]
  *                  (a tight parent), pred[src] = src.
  *
+ *   oracle_bc   -- bc[v] = sum over the given sources s of Brandes's dependency
+ *                  delta_s(v) = sum over t != s, v of sigma_st(v) / sigma_st,
+ *                  with shortest = fewest CSR out-edges (no halving).
+ *                  Paper §5.3 names Brandes's formulation
+ *                  ("a forward BFS pass to accumulate sigma values for each
+ *                  node, and a backward BFS pass to compute centrality
+ *                  values"). Algorithm: Brandes 2001, Algorithm 1, as printed
+ *                  (FIFO BFS with a stack S and predecessor lists P[w]; then
+ *                  pop w, delta[v] += sigma[v]/sigma[w] * (1 + delta[w]) for
+ *                  v in P[w]; bc[w] += delta[w] for w != s), in double.
+ *
  * Return codes: 0 ok, 1 bad argument (src out of range / n <= 0),
  * 2 out of memory, 3 a distance does not fit in uint32 (reading A-19).
  */
@@ -137,4 +148,65 @@ int oracle_sssp(int64_t n, const int64_t *R, const int32_t *C, const uint32_t *W
     }
     free(dist); free(done); free(heap);
     return rc;
+}
+
+int oracle_bc(int64_t n, const int64_t *R, const int32_t *C, const int32_t *sources, int64_t nsrc,
+              double *bc)
+{
+    if (n <= 0 || nsrc < 0) return 1;
+    for (int64_t i = 0; i < nsrc; ++i)
+        if (sources[i] < 0 || sources[i] >= n) return 1;
+    int64_t m = R[n];
+    int32_t *S = (int32_t *)malloc((size_t)n * sizeof(int32_t));      /* stack (= BFS order) */
+    int64_t *dist = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    double *sigma = (double *)malloc((size_t)n * sizeof(double));
+    double *delta = (double *)malloc((size_t)n * sizeof(double));
+    int64_t *phead = (int64_t *)malloc((size_t)n * sizeof(int64_t));  /* P[w]: linked lists */
+    int64_t *pnext = (int64_t *)malloc((size_t)(m > 0 ? m : 1) * sizeof(int64_t));
+    int32_t *pv = (int32_t *)malloc((size_t)(m > 0 ? m : 1) * sizeof(int32_t));
+    if (!S || !dist || !sigma || !delta || !phead || !pnext || !pv) {
+        free(S); free(dist); free(sigma); free(delta); free(phead); free(pnext); free(pv);
+        return 2;
+    }
+    for (int64_t v = 0; v < n; ++v) bc[v] = 0.0;
+    for (int64_t i = 0; i < nsrc; ++i) {
+        int32_t s = sources[i];
+        int64_t np = 0, top = 0, head = 0;
+        for (int64_t v = 0; v < n; ++v) {
+            phead[v] = -1;
+            sigma[v] = 0.0;
+            dist[v] = -1;
+        }
+        sigma[s] = 1.0;
+        dist[s] = 0;
+        /* the queue is S itself: S[head..top) are enqueued, S[0..top) is the stack */
+        S[top++] = s;
+        while (head < top) {
+            int32_t v = S[head++];
+            for (int64_t e = R[v]; e < R[v + 1]; ++e) {
+                int32_t w = C[e];
+                if (dist[w] < 0) {             /* w found for the first time? */
+                    S[top++] = w;
+                    dist[w] = dist[v] + 1;
+                }
+                if (dist[w] == dist[v] + 1) {  /* shortest path to w via v? */
+                    sigma[w] += sigma[v];
+                    pv[np] = v;                /* append v to P[w] */
+                    pnext[np] = phead[w];
+                    phead[w] = np++;
+                }
+            }
+        }
+        for (int64_t v = 0; v < n; ++v) delta[v] = 0.0;
+        while (top > 0) {                      /* S returns vertices in order of non-increasing distance */
+            int32_t w = S[--top];
+            for (int64_t k = phead[w]; k >= 0; k = pnext[k]) {
+                int32_t v = pv[k];
+                delta[v] += sigma[v] / sigma[w] * (1.0 + delta[w]);
+            }
+            if (w != s) bc[w] += delta[w];
+        }
+    }
+    free(S); free(dist); free(sigma); free(delta); free(phead); free(pnext); free(pv);
+    return 0;
 }

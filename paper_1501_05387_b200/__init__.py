@@ -74,7 +74,7 @@ EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_gra
            "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_shard",
            "gr_part_bfs_pull", "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
            "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_far_min",
-           "gr_part_sssp_resplit", "gr_part_sssp_end"]
+           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc"]
 
 
 def load(path: str = LIB_PATH):
@@ -125,6 +125,7 @@ def load(path: str = LIB_PATH):
     lib.gr_part_sssp_far_min.argtypes = [p, i32, i32, u64, P(u64)]
     lib.gr_part_sssp_resplit.argtypes = [p, i32, i32, i32, u64, u64]
     lib.gr_part_sssp_end.argtypes = [p]
+    lib.gr_bc.argtypes = [p, p, i64, p, p]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
               "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
               "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
@@ -132,7 +133,7 @@ def load(path: str = LIB_PATH):
               "gr_part_bfs_frontier", "gr_part_bfs_shard", "gr_part_bfs_pull",
               "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
               "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts",
-              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end"):
+              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -290,6 +291,20 @@ class Graph:
         pp, _ = _ptr(pred)
         (gr_sssp_async if asynchronous else gr_sssp)(self.handle, src, dp, pp, o)
         return dist, pred
+
+    def bc(self, sources, bc=None, sigma=None):
+        """Betweenness centrality (Brandes): bc[v] = sum over the
+        given sources s of the dependency delta_s(v) (fp64; no halving -- for
+        a symmetric graph over all sources Brandes's value is bc / 2)."""
+        import numpy as np
+        import torch
+        src = np.ascontiguousarray(np.asarray(list(sources), dtype=np.int32))
+        if bc is None:
+            bc = torch.empty(self.n, dtype=torch.float64, device=torch.device("cuda", self.device))
+        bp, _ = _ptr(bc)
+        sp, _ = _ptr(sigma)
+        _check(load().gr_bc(self.handle, src.ctypes.data_as(ctypes.c_void_p), int(src.size), bp, sp))
+        return bc
 
     def sync(self):
         """Wait for the asynchronous runs of this graph; raises on a queue overflow."""

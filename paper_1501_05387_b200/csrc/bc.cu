@@ -1,0 +1,268 @@
+// bc.cu -- betweenness centrality, Brandes's two-pass formulation as the
+// paper's second consumer of the advance operator.
+//
+// Paper §5.3: "The first phase has an advance step identical to
+// the original BFS and a computation step that computes the number of
+// shortest paths from source to each vertex. The second phase uses an
+// advance step to iterate over the BFS frontier backwards with a computation
+// step to compute the dependency scores." Brandes (cited P:962-963):
+//   sigma[s] = 1, sigma[w] = sum over (v,w) in E with d[w] = d[v]+1 of sigma[v]
+//   delta[v] = sum over (v,w) in E with d[w] = d[v]+1 of sigma[v]/sigma[w] (1 + delta[w])
+//   bc[v]   += delta[v]  for v != s.
+//
+// B200 design:
+//  * forward level L: merge-path advance (expand_lb) over the level-L queue;
+//    per edge (v,w): claim w by CAS on depth (-1 -> L+1, the winner appends
+//    w to the level-(L+1) queue with its degree prefix), and every edge whose
+//    target sits at L+1 adds sigma[v] (carried as the window payload) with a
+//    double atomicAdd ("atomicAdd" accumulation);
+//  * the queues of all levels are kept back to back (each vertex is appended
+//    exactly once, so n entries suffice) -- the "BFS frontier" the second
+//    phase iterates backwards (SPEC S:445 reading: retained frontiers);
+//  * backward level L (deepest first): the same advance over the level-L
+//    queue, each edge (v,w) with d[w] = L+1 contributes sigma[v]/sigma[w]
+//    (1 + delta[w]) to delta[v]; a warp whose 32 edges share v (long lists:
+//    the common case on hubs) reduces in registers and issues one atomic.
+// sigma / delta / bc are fp64 (the oracle's precision; path counts exceed
+// fp32's 24-bit mantissa on the paper's graphs).
+#include <vector>
+
+#include "frontier.cuh"
+
+namespace gr {
+
+bool ptr_on_device(const void *p);
+
+constexpr int kBcBlock = 256;
+constexpr int kBcWarps = kBcBlock / 32;
+constexpr int kBcStage = 64;
+using BcAppender = AppenderT<kBcStage>;
+
+struct BcArgs {
+    int64_t n;
+    const int64_t *R;
+    const int32_t *C;
+    int32_t *depth;
+    double *sigma;
+    double *delta;
+    int32_t *qv;               // all levels back to back
+    int64_t *qo;
+    int64_t *qr;
+    unsigned long long *cnt;   // per level: (edges << S) | count
+    int S;
+};
+
+struct BcFwdOp {
+    const BcArgs *a;
+    int32_t next;              // L + 1
+    BcAppender *app;
+
+    __device__ __forceinline__ unsigned long long entry(int32_t v) {
+        return (unsigned long long)__double_as_longlong(__ldcg(a->sigma + v));
+    }
+
+    template <int U, class T5>
+    __device__ __forceinline__ void edges(const bool *ok, const int32_t *, const unsigned long long *pay,
+                                          const int32_t *dst, const T5 *) {
+        int32_t d[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d[u] = ok[u] ? __ldcg(a->depth + dst[u]) : -2;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int32_t w = dst[u];
+            bool disc = false;
+            int64_t deg = 0, rs = 0;
+            int32_t dw = d[u];
+            if (dw == -1) {
+                dw = atomicCAS(a->depth + w, -1, next);
+                disc = dw == -1;
+                if (disc) dw = next;
+            }
+            if (dw == next) atomicAdd(a->sigma + w, __longlong_as_double((long long)pay[u]));
+            if (disc) { rs = a->R[w]; deg = a->R[w + 1] - rs; }
+            app->push(disc && deg > 0, w, deg, rs);
+        }
+    }
+};
+
+struct BcBwdOp {
+    const BcArgs *a;
+    int32_t next;              // L + 1
+
+    __device__ __forceinline__ unsigned long long entry(int32_t v) {
+        return (unsigned long long)__double_as_longlong(__ldcg(a->sigma + v));
+    }
+
+    template <int U, class T5>
+    __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *pay,
+                                          const int32_t *dst, const T5 *) {
+        int32_t d[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) d[u] = ok[u] ? __ldcg(a->depth + dst[u]) : -2;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double c = 0.0;
+            if (d[u] == next) {  // w is a successor of v on a shortest path
+                const int32_t w = dst[u];
+                c = __longlong_as_double((long long)pay[u]) / __ldcg(a->sigma + w) * (1.0 + __ldcg(a->delta + w));
+            }
+            const int32_t s0 = __shfl_sync(0xffffffffu, src[u], 0);
+            if (__all_sync(0xffffffffu, src[u] == s0)) {
+                c = warp_sum<double>(c);
+                if (lane_id() == 0 && c != 0.0) atomicAdd(a->delta + s0, c);
+            } else if (c != 0.0) {
+                atomicAdd(a->delta + src[u], c);
+            }
+        }
+    }
+};
+
+__global__ void bc_init_kernel(BcArgs a, int32_t s) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < a.n; v += nt) {
+        a.depth[v] = v == s ? 0 : -1;
+        a.sigma[v] = v == s ? 1.0 : 0.0;
+        a.delta[v] = 0.0;
+    }
+    if (tid == 0) {
+        const int64_t d = a.R[s + 1] - a.R[s];
+        a.qv[0] = s;
+        a.qo[0] = 0;
+        a.qr[0] = a.R[s];
+        a.cnt[0] = d > 0 ? (((unsigned long long)d << a.S) | 1ull) : 0ull;
+        a.cnt[1] = 0ull;
+    }
+}
+
+__global__ void __launch_bounds__(kBcBlock) bc_fwd_kernel(BcArgs a, int L, int64_t off, int64_t f, int64_t mf) {
+    __shared__ int32_t s_v[kBcWarps][kBcStage];
+    __shared__ int32_t s_d[kBcWarps][kBcStage];
+    __shared__ int64_t s_r[kBcWarps][kBcStage];
+    const int wib = threadIdx.x >> 5;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[L + 2] = 0ull;  // read by level L+1
+    BcAppender app;
+    app.sv = s_v[wib]; app.sd = s_d[wib]; app.sr = s_r[wib]; app.cnt = 0; app.S = a.S;
+    app.cap = a.n - (off + f);
+    app.overflow = a.cnt + a.n + 2;  // never set: each vertex is appended once
+    app.qv = a.qv + off + f;
+    app.qo = a.qo + off + f;
+    app.qr = a.qr + off + f;
+    app.counter = a.cnt + L + 1;
+    BcFwdOp op{&a, L + 1, &app};
+    GlobalFrontier fr{a.qv + off, a.qo + off, a.qr + off, f, mf};
+    expand_lb(fr, a.C, gw, nw, op);
+    app.finish();
+}
+
+__global__ void __launch_bounds__(kBcBlock) bc_bwd_kernel(BcArgs a, int L, int64_t off, int64_t f, int64_t mf) {
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    BcBwdOp op{&a, L + 1};
+    GlobalFrontier fr{a.qv + off, a.qo + off, a.qr + off, f, mf};
+    expand_lb(fr, a.C, gw, nw, op);
+}
+
+__global__ void bc_accum_kernel(const double *delta, int64_t n, int32_t s, double *bc) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < n; v += nt)
+        if (v != s) bc[v] += delta[v];
+}
+
+__global__ void bc_zero_kernel(double *x, int64_t n) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < n; v += nt) x[v] = 0.0;
+}
+
+}  // namespace gr
+
+using namespace gr;
+
+extern "C" {
+
+gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out) {
+    Graph *g = (Graph *)h;
+    if (!g || !bc_out || nsrc < 0 || (nsrc > 0 && !sources)) {
+        set_error("graph / bc_out / sources is NULL or nsrc < 0");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    if (g->part) { set_error("gr_bc needs a whole (unpartitioned) graph"); return GR_ERR_INVALID_ARGUMENT; }
+    if (ptr_on_device(sources)) { set_error("sources must be host memory"); return GR_ERR_INVALID_ARGUMENT; }
+    for (int64_t i = 0; i < nsrc; ++i)
+        if (sources[i] < 0 || sources[i] >= g->n) {
+            set_error("sources[%lld]=%d not in [0, n=%lld)", (long long)i, sources[i], (long long)g->n);
+            return GR_ERR_OUT_OF_RANGE;
+        }
+    GR_CUDA(cudaSetDevice(g->device));
+    if (g->pending && gr_graph_sync(h) != GR_OK) return GR_ERR_OVERFLOW;
+    gr_status st;
+    const int64_t n = g->n;
+    if (!g->bc_sigma) {
+        if ((st = dev_alloc(g, (void **)&g->bc_depth, n * sizeof(int32_t))) != GR_OK ||
+            (st = dev_alloc(g, (void **)&g->bc_sigma, n * sizeof(double))) != GR_OK ||
+            (st = dev_alloc(g, (void **)&g->bc_delta, n * sizeof(double))) != GR_OK ||
+            (st = dev_alloc(g, (void **)&g->bc_cnt, (n + 3) * sizeof(unsigned long long))) != GR_OK)
+            return st;
+    }
+    const bool dev_bc = ptr_on_device(bc_out);
+    double *bc = bc_out;
+    if (!dev_bc) {
+        if (!g->bc_buf && (st = dev_alloc(g, (void **)&g->bc_buf, n * sizeof(double))) != GR_OK) return st;
+        bc = g->bc_buf;
+    }
+    BcArgs a;
+    a.n = n; a.R = g->R; a.C = g->C;
+    a.depth = g->bc_depth; a.sigma = g->bc_sigma; a.delta = g->bc_delta;
+    a.qv = g->qv[0]; a.qo = g->qo[0]; a.qr = g->qr[0];
+    a.cnt = g->bc_cnt; a.S = g->pack_shift;
+    const int grid = g->num_sms * 8;
+    cudaStream_t s = g->stream;
+    bc_zero_kernel<<<g->num_sms * 4, 256, 0, s>>>(bc, n);
+    int launches = 1;
+    std::vector<int64_t> off, fs, mfs;
+    int levels_total = 0;
+    for (int64_t i = 0; i < nsrc; ++i) {
+        const int32_t src = sources[i];
+        bc_init_kernel<<<g->num_sms * 4, 256, 0, s>>>(a, src);
+        ++launches;
+        off.assign(1, 0);
+        fs.clear();
+        mfs.clear();
+        for (int L = 0;; ++L) {  // forward phase: BFS + sigma (one host read per level)
+            unsigned long long qp = 0;
+            GR_CUDA(cudaMemcpyAsync(&qp, a.cnt + L, sizeof(qp), cudaMemcpyDeviceToHost, s));
+            GR_CUDA(cudaStreamSynchronize(s));
+            const int64_t f = (int64_t)(qp & ((1ull << a.S) - 1)), mf = (int64_t)(qp >> a.S);
+            if (f == 0) break;
+            fs.push_back(f);
+            mfs.push_back(mf);
+            bc_fwd_kernel<<<grid, kBcBlock, 0, s>>>(a, L, off[L], f, mf);
+            ++launches;
+            off.push_back(off[L] + f);
+        }
+        levels_total += (int)fs.size();
+        // backward phase: the stored frontiers, deepest first (level 0 = the
+        // source, whose delta is not accumulated but is cheap to compute)
+        for (int L = (int)fs.size() - 1; L >= 1; --L) {
+            bc_bwd_kernel<<<grid, kBcBlock, 0, s>>>(a, L, off[L], fs[L], mfs[L]);
+            ++launches;
+        }
+        bc_accum_kernel<<<g->num_sms * 4, 256, 0, s>>>(a.delta, n, src, bc);
+        ++launches;
+    }
+    GR_CUDA(cudaGetLastError());
+    if (!dev_bc) GR_CUDA(cudaMemcpyAsync(bc_out, bc, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (sigma_out && nsrc > 0) GR_CUDA(cudaMemcpyAsync(sigma_out, a.sigma, n * sizeof(double), cudaMemcpyDefault, s));
+    GR_CUDA(cudaStreamSynchronize(s));
+    count_launch(launches);
+    g->last_launches = launches;
+    g->stats_levels = levels_total;
+    g->stats_records = -1;  // no per-level records for BC
+    return GR_OK;
+}
+
+}  // extern "C"

@@ -138,6 +138,10 @@ struct Graph {
     int32_t *ps_recv = nullptr;             // [3 * nparts * block]
     uint32_t *ps_dist = nullptr;            // caller's outputs (gr_part_sssp_begin)
     int32_t *ps_pred = nullptr;
+    // betweenness centrality (bc.cu)
+    int32_t *bc_depth = nullptr;
+    double *bc_sigma = nullptr, *bc_delta = nullptr, *bc_buf = nullptr;
+    unsigned long long *bc_cnt = nullptr;   // [n + 3] per-level packed counters
 };
 
 gr_status dev_alloc(Graph *g, void **p, size_t bytes);
