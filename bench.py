@@ -54,6 +54,8 @@ PAPER_CONTEXT = {  # Table 3, K40c, real datasets: context only
     ("c3_orkut", "sssp"): "Gunrock SSSP soc-orkut on K40c: 1088 ms, 0.1955 GTEPS (P:1152-1153)",
     ("c4_road", "bfs"): "Gunrock BFS roadnet_CA (11x fewer edges) on K40c: 0.178 GTEPS (P:1150-1151)",
     ("c4_road", "sssp"): "Gunrock SSSP roadnet_CA on K40c: 0.0249 GTEPS (P:1162-1163)",
+    ("c2_kron21", "bc"): "Gunrock BC kron_g500-logn21 on K40c: 716.1 ms, 0.5085 GTEPS as 2|E|/t (P:1164-1171)",
+    ("c3_orkut", "bc"): "Gunrock BC soc-orkut on K40c: 721.2 ms, 0.5898 GTEPS as 2|E|/t (P:1164-1165)",
 }
 
 
@@ -63,7 +65,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2_kron21", choices=sorted(CONFIG_DESC))
-    ap.add_argument("--prim", default="bfs", choices=["bfs", "sssp"])
+    ap.add_argument("--prim", default="bfs", choices=["bfs", "sssp", "bc"])
     ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
     ap.add_argument("--delta", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -200,21 +202,28 @@ def run_reference(args, rank, world):
     edges, secs = 0, 0.0
     for i, s in enumerate(srcs):
         t0 = time.perf_counter()
+        mult = 1
         if args.prim == "bfs":
             x, _ = oracle.bfs(R, C, s, want_pred=True)
             unreached = -1
+        elif args.prim == "bc":
+            oracle.bc(R, C, [s])
+            dt = time.perf_counter() - t0
+            x, _ = oracle.bfs(R, C, s, want_pred=False)  # untimed: reached edges
+            unreached, mult = -1, 2                         # BC TEPS = 2 m_reached / t
         else:
             x, _ = oracle.sssp(R, C, W, s, want_pred=True)
             unreached = oracle.UINT32_MAX
-        dt = time.perf_counter() - t0
+        if args.prim != "bc":
+            dt = time.perf_counter() - t0
         if i >= args.warmup:
-            edges += oracle.reached_edges(R, x, unreached)
+            edges += mult * oracle.reached_edges(R, x, unreached)
             secs += dt
     value = edges / secs / 1e9
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-           "dtype": "int32" if args.prim == "bfs" else "u32", "data": "synthetic",
+           "dtype": {"bfs": "int32", "sssp": "u32", "bc": "f64"}[args.prim], "data": "synthetic",
            "config": {"workload": "%s %s" % (args.config, args.prim), "graph": CONFIG_DESC[args.config],
                       "n": g.n, "m": g.m},
            "cpu_baseline": {"value": value, "unit": "GTEPS", "cores": 1, "kind": "oracle",
@@ -313,6 +322,122 @@ def run_partitioned(args, rank, world, dev):
     dist.destroy_process_group()
 
 
+def run_bc(args, rank, world, dev):
+    """Betweenness centrality: one step = the Brandes
+    forward + backward passes of one source (gr_bc, synchronous: one host
+    read per level, so the events include those bubbles). TEPS = 2 m_reached
+    / t (the paper's BC convention, both passes traverse the edges).
+    Replicas: sources sharded over the ranks."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import graphgen as gg
+    import paper_1501_05387_b200 as gr
+    g = gg.make_config(args.config, device=dev)
+    G = gr.Graph(g.R, g.C, None, symmetric=True)
+    deg = g.R[1:] - g.R[:-1]
+    n, m = g.n, g.m
+    srcs = gg.sources(g, args.warmup + args.steps * world)
+    mine = srcs[args.warmup + rank * args.steps: args.warmup + (rank + 1) * args.steps]
+    bcv = torch.empty(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for s in srcs[: args.warmup]:
+        G.bc([s], bc=bcv)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = gr.gr_kernel_launch_count()
+    ms = []
+    with Clocks(local_index(dev)) as clk:
+        for s in mine:
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            G.bc([s], bc=bcv)
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+    launches = gr.gr_kernel_launch_count() - l0
+    # untimed: reached edges / vertices of each source (BFS depth) for TEPS and the byte model
+    depth = torch.empty(n, dtype=torch.int32, device=dev)
+    edges, byts = 0, []
+    for s in mine:
+        G.bfs(s, depth, None)
+        r = depth >= 0
+        mr, nr, q = int(deg[r].sum()), int(r.sum()), int((r & (deg > 0)).sum())
+        edges += 2 * mr
+        # init 20n + fwd (20 Q + 4 m_r + 24 n_r) + bwd (20 Q + 4 m_r + 8 Q) + accumulate 24 n
+        byts.append(20 * n + 20 * q + 4 * mr + 24 * nr + 28 * q + 4 * mr + 24 * n)
+    tot = sum(ms)
+    if world > 1:
+        t = torch.tensor([tot, float(edges)], dtype=torch.float64, device=dev)
+        tm = t[:1].clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:])
+        tot_all, edges_all = float(tm[0]), float(t[1])
+    else:
+        tot_all, edges_all = tot, float(edges)
+    peak, peak_src = load_peaks()
+    achieved = sum(byts) / (tot * 1e-3) / 1e9
+    workload = "%s bc (Brandes, one source per step)" % args.config
+    out = {"metric": METRIC, "value": edges_all / (tot_all * 1e-3) / 1e9, "unit": "GTEPS", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_all / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": workload, "graph": CONFIG_DESC[args.config], "n": n, "m": m,
+                      "sources": "%d seeded sources with degree>=1 per rank (S:519)" % args.steps,
+                      "teps": "2 m_reached / t (paper's BC convention, P:1164-1171)",
+                      "l2": "flushed (256 MiB write) between timed steps",
+                      "parallelism": "replicas: sources sharded over %d rank(s)" % world},
+           "roofline": {"bound": "hbm", "kernel": "bc_fwd_kernel+bc_bwd_kernel", "achieved": achieved,
+                        "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                        "peak_source": peak_src,
+                        "model": "init 20n + fwd 20Q+4m_r+24n_r + bwd 28Q+4m_r + accumulate 24n "
+                                 "(Q = reached vertices with out-degree > 0)"},
+           "gpu_launches": launches, "paper_context": PAPER_CONTEXT.get((args.config, "bc"))}
+    if rank == 0:
+        out["clocks"] = clk.summary()
+    # end to end: host (pinned) output buffer through the C ABI
+    pin = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    G.bc(mine[:1], bc=pin)
+    e2e_s = 0.0
+    for s in mine:
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        G.bc([s], bc=pin)
+        e2e_s += time.perf_counter() - t0
+    out["e2e"] = {"value": edges / e2e_s / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 4,
+                  "d2h_bytes_per_step": 8 * n,
+                  "what": "gr_bc through the C ABI writing a host (pinned) bc array; host wall clock per call"}
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        R, C, _ = g.numpy()
+        ce, cs, cnt = 0, 0.0, 0
+        for s in mine:
+            t0 = time.perf_counter()
+            oracle.bc(R, C, [s])
+            cs += time.perf_counter() - t0
+            d, _ = oracle.bfs(R, C, s)
+            ce += 2 * oracle.reached_edges(R, d, -1)
+            cnt += 1
+            if cs > args.cpu_sample_s:
+                break
+        out["cpu_baseline"] = {"value": ce / cs / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                               "sample": "%d of the timed sources, full Brandes single-source passes of %s, "
+                                         "single-threaded C oracle (%d host cores available)"
+                                         % (cnt, args.config, os.cpu_count())}
+    if rank == 0:
+        emit(out)
+    G.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def local_index(dev):
+    return dev.index if dev.index is not None else 0
+
+
 # ----------------------------------------------------------------- our arm
 
 def main():
@@ -336,6 +461,8 @@ def main():
     dev = torch.device("cuda", local)
     if args.partitioned:
         return run_partitioned(args, rank, world, dev)
+    if args.prim == "bc":
+        return run_bc(args, rank, world, dev)
     want_w = args.prim == "sssp"
     g = gg.make_config(args.config, device=dev, weights=want_w or None)
     G = gr.Graph(g.R, g.C, g.W if want_w else None, symmetric=True)
