@@ -238,6 +238,19 @@ const char *gr_version(void);
 gr_status gr_bc(gr_graph *g, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out);
 
 /* ===========================================================================
+ * Connected components (paper §5.4: hooking on
+ * an edge frontier with a filter removing edges whose endpoints share a
+ * component ID, then pointer jumping "until it reaches the root").
+ *   comp_out[v] = the smallest vertex id of v's connected component (edges
+ *   taken as undirected: weak components of a directed CSR). The canonical
+ *   min-id label is reading A-22 (hooking always points the larger root at
+ *   the smaller).
+ * comp_out: int32[n], host or device (overwritten). num_components: host
+ * int64 or NULL. Synchronous (one host read per hooking pass).
+ * =========================================================================== */
+gr_status gr_cc(gr_graph *g, int32_t *comp_out, int64_t *num_components);
+
+/* ===========================================================================
  * Multi-GPU: 1D vertex partition (the paper is single-GPU and
  * lists multi-GPU as future work). One process per GPU. Rank q of
  * P owns the contiguous vertex block [q*B, min(n, (q+1)*B)), B = 32*ceil(n/(32P))

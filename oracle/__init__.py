@@ -9,6 +9,7 @@ Contents
 * bfs(R, C, src)        -> (depth int32[n], pred int32[n])  FIFO-queue BFS (oracle.c)
 * sssp(R, C, W, src)    -> (dist uint32[n], pred int32[n])  binary-heap Dijkstra (oracle.c)
 * bc(R, C, sources)     -> float64[n]  Brandes 2001 Algorithm 1 (oracle.c)
+* cc(R, C)              -> (comp int32[n], count)  union-find, min id per component
 * check_bfs / check_sssp -- O(m) certificates: they decide
   exactness of depth / dist without any reference output, and validate any
   predecessor array (pred is "any valid parent": parity-unpinned by design,
@@ -54,6 +55,8 @@ def _load():
         lib.oracle_sssp.restype = ctypes.c_int
         lib.oracle_bc.argtypes = [ctypes.c_int64, p, p, p, ctypes.c_int64, p]
         lib.oracle_bc.restype = ctypes.c_int
+        lib.oracle_cc.argtypes = [ctypes.c_int64, p, p, p, p]
+        lib.oracle_cc.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -104,6 +107,19 @@ def bc(R, C, sources):
     if rc != 0:
         raise ValueError("oracle_bc failed with code %d" % rc)
     return out
+
+
+def cc(R, C):
+    """(comp, count): comp[v] = smallest vertex id of v's weakly connected component."""
+    R = _as(R, np.int64)
+    C = _as(C, np.int32)
+    n = R.size - 1
+    comp = np.empty(n, np.int32)
+    k = np.zeros(1, np.int64)
+    rc = _load().oracle_cc(n, _ptr(R), _ptr(C), _ptr(comp), _ptr(k))
+    if rc != 0:
+        raise ValueError("oracle_cc failed with code %d" % rc)
+    return comp, int(k[0])
 
 
 # ---------------------------------------------------------------------------

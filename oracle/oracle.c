@@ -35,6 +35,14 @@
  *                  pop w, delta[v] += sigma[v]/sigma[w] * (1 + delta[w]) for
  *                  v in P[w]; bc[w] += delta[w] for w != s), in double.
  *
+ *   oracle_cc   -- comp[v] = the smallest vertex id of v's (weakly) connected
+ *                  component, edges taken as undirected; returns the number
+ *                  of components in *ncomp. Paper §5.4: "labels
+ *                  the vertices in each connected component in a graph with a
+ *                  unique component ID". Algorithm: textbook disjoint-set
+ *                  union (union by size, path halving) over every CSR edge,
+ *                  then the minimum id of each set.
+ *
  * Return codes: 0 ok, 1 bad argument (src out of range / n <= 0),
  * 2 out of memory, 3 a distance does not fit in uint32 (reading A-19).
  */
@@ -208,5 +216,42 @@ int oracle_bc(int64_t n, const int64_t *R, const int32_t *C, const int32_t *sour
         }
     }
     free(S); free(dist); free(sigma); free(delta); free(phead); free(pnext); free(pv);
+    return 0;
+}
+
+static int32_t uf_find(int32_t *parent, int32_t x)
+{
+    while (parent[x] != x) {
+        parent[x] = parent[parent[x]]; /* path halving */
+        x = parent[x];
+    }
+    return x;
+}
+
+int oracle_cc(int64_t n, const int64_t *R, const int32_t *C, int32_t *comp, int64_t *ncomp)
+{
+    if (n <= 0) return 1;
+    int32_t *parent = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    int64_t *size = (int64_t *)malloc((size_t)n * sizeof(int64_t));
+    int32_t *minid = (int32_t *)malloc((size_t)n * sizeof(int32_t));
+    if (!parent || !size || !minid) { free(parent); free(size); free(minid); return 2; }
+    for (int64_t v = 0; v < n; ++v) { parent[v] = (int32_t)v; size[v] = 1; }
+    for (int64_t u = 0; u < n; ++u)
+        for (int64_t e = R[u]; e < R[u + 1]; ++e) {
+            int32_t a = uf_find(parent, (int32_t)u), b = uf_find(parent, C[e]);
+            if (a == b) continue;
+            if (size[a] < size[b]) { int32_t t = a; a = b; b = t; }
+            parent[b] = a;               /* union by size */
+            size[a] += size[b];
+        }
+    for (int64_t v = 0; v < n; ++v) minid[v] = INT32_MAX;
+    int64_t k = 0;
+    for (int64_t v = 0; v < n; ++v) {   /* increasing v: the first member seen is the minimum */
+        int32_t r = uf_find(parent, (int32_t)v);
+        if (minid[r] == INT32_MAX) { minid[r] = (int32_t)v; ++k; }
+        comp[v] = minid[r];
+    }
+    *ncomp = k;
+    free(parent); free(size); free(minid);
     return 0;
 }

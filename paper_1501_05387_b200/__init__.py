@@ -74,7 +74,7 @@ EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_gra
            "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_shard",
            "gr_part_bfs_pull", "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
            "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_far_min",
-           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc"]
+           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc"]
 
 
 def load(path: str = LIB_PATH):
@@ -126,6 +126,7 @@ def load(path: str = LIB_PATH):
     lib.gr_part_sssp_resplit.argtypes = [p, i32, i32, i32, u64, u64]
     lib.gr_part_sssp_end.argtypes = [p]
     lib.gr_bc.argtypes = [p, p, i64, p, p]
+    lib.gr_cc.argtypes = [p, p, P(i64)]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
               "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
               "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
@@ -133,7 +134,7 @@ def load(path: str = LIB_PATH):
               "gr_part_bfs_frontier", "gr_part_bfs_shard", "gr_part_bfs_pull",
               "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
               "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts",
-              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc"):
+              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -305,6 +306,17 @@ class Graph:
         sp, _ = _ptr(sigma)
         _check(load().gr_bc(self.handle, src.ctypes.data_as(ctypes.c_void_p), int(src.size), bp, sp))
         return bc
+
+    def cc(self, comp=None):
+        """Connected components: (comp, count), comp[v] = the
+        smallest vertex id of v's (weak) component."""
+        import torch
+        if comp is None:
+            comp = torch.empty(self.n, dtype=torch.int32, device=torch.device("cuda", self.device))
+        cp, _ = _ptr(comp)
+        k = ctypes.c_int64()
+        _check(load().gr_cc(self.handle, cp, ctypes.byref(k)))
+        return comp, k.value
 
     def sync(self):
         """Wait for the asynchronous runs of this graph; raises on a queue overflow."""

@@ -142,6 +142,9 @@ struct Graph {
     int32_t *bc_depth = nullptr;
     double *bc_sigma = nullptr, *bc_delta = nullptr, *bc_buf = nullptr;
     unsigned long long *bc_cnt = nullptr;   // [n + 3] per-level packed counters
+    // connected components (cc.cu)
+    unsigned long long *cc_ctl = nullptr;   // survivors, changed, count
+    int2 *cc_list[2] = {nullptr, nullptr};  // edge frontier ping-pong
 };
 
 gr_status dev_alloc(Graph *g, void **p, size_t bytes);
