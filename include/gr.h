@@ -251,6 +251,21 @@ gr_status gr_bc(gr_graph *g, const int32_t *sources, int64_t nsrc, double *bc_ou
 gr_status gr_cc(gr_graph *g, int32_t *comp_out, int64_t *num_components);
 
 /* ===========================================================================
+ * PageRank (paper §5.5: a frontier of all
+ * vertices, one advance computing PageRank on the frontier, one filter
+ * removing converged vertices, AtomicAdd accumulation). Reading A-23:
+ *   PR(v) = (1 - damping)/n + damping * sum over in-edges (u,v) of PR(u)/outdeg(u)
+ * from PR = 1/n, no dangling-mass redistribution; a vertex leaves the
+ * frontier when |PR_new(v) - PR_old(v)| <= tol * PR_new(v); stops when the
+ * frontier is empty or after max_iter steps.
+ * damping in [0,1), tol >= 0, max_iter >= 1 (GR_ERR_INVALID_ARGUMENT).
+ * rank_out: double[n], host or device. iterations: host int32 or NULL.
+ * In-edges come from the CSC (the CSR itself for GR_SYMMETRIC graphs).
+ * =========================================================================== */
+gr_status gr_pagerank(gr_graph *g, double damping, double tol, int32_t max_iter, double *rank_out,
+                      int32_t *iterations);
+
+/* ===========================================================================
  * Multi-GPU: 1D vertex partition (the paper is single-GPU and
  * lists multi-GPU as future work). One process per GPU. Rank q of
  * P owns the contiguous vertex block [q*B, min(n, (q+1)*B)), B = 32*ceil(n/(32P))

@@ -10,6 +10,7 @@ Contents
 * sssp(R, C, W, src)    -> (dist uint32[n], pred int32[n])  binary-heap Dijkstra (oracle.c)
 * bc(R, C, sources)     -> float64[n]  Brandes 2001 Algorithm 1 (oracle.c)
 * cc(R, C)              -> (comp int32[n], count)  union-find, min id per component
+* pagerank(R, C, d)     -> float64[n]  Jacobi power iteration in numpy (reading A-23)
 * check_bfs / check_sssp -- O(m) certificates: they decide
   exactness of depth / dist without any reference output, and validate any
   predecessor array (pred is "any valid parent": parity-unpinned by design,
@@ -120,6 +121,28 @@ def cc(R, C):
     if rc != 0:
         raise ValueError("oracle_cc failed with code %d" % rc)
     return comp, int(k[0])
+
+
+def pagerank(R, C, damping: float = 0.85, tol: float = 1e-15, max_iter: int = 100000):
+    """PR(v) = (1-d)/n + d * sum over edges (u,v) of PR(u)/outdeg(u), start 1/n,
+    no dangling redistribution (paper §5.5; reading A-23).
+    Plain Jacobi power iteration in fp64 until max |PR_new - PR| <= tol * max PR."""
+    R = _as(R, np.int64)
+    C = _as(C, np.int64)
+    n = R.size - 1
+    outdeg = np.diff(R)
+    src = np.repeat(np.arange(n), outdeg)
+    x = np.full(n, 1.0 / n)
+    for _ in range(max_iter):
+        share = np.zeros(n)
+        nz = outdeg > 0
+        share[nz] = x[nz] / outdeg[nz]
+        y = (1.0 - damping) / n + damping * np.bincount(C, weights=share[src], minlength=n)
+        done = np.abs(y - x).max() <= tol * y.max()
+        x = y
+        if done:
+            break
+    return x
 
 
 # ---------------------------------------------------------------------------

@@ -74,7 +74,7 @@ EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_gra
            "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_shard",
            "gr_part_bfs_pull", "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
            "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_far_min",
-           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc"]
+           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank"]
 
 
 def load(path: str = LIB_PATH):
@@ -127,6 +127,7 @@ def load(path: str = LIB_PATH):
     lib.gr_part_sssp_end.argtypes = [p]
     lib.gr_bc.argtypes = [p, p, i64, p, p]
     lib.gr_cc.argtypes = [p, p, P(i64)]
+    lib.gr_pagerank.argtypes = [p, ctypes.c_double, ctypes.c_double, i32, p, P(i32)]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
               "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
               "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
@@ -134,7 +135,7 @@ def load(path: str = LIB_PATH):
               "gr_part_bfs_frontier", "gr_part_bfs_shard", "gr_part_bfs_pull",
               "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
               "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts",
-              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc"):
+              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -317,6 +318,16 @@ class Graph:
         k = ctypes.c_int64()
         _check(load().gr_cc(self.handle, cp, ctypes.byref(k)))
         return comp, k.value
+
+    def pagerank(self, damping: float = 0.85, tol: float = 1e-10, max_iter: int = 1000, rank=None):
+        """PageRank (reading A-23): (rank float64[n], iterations)."""
+        import torch
+        if rank is None:
+            rank = torch.empty(self.n, dtype=torch.float64, device=torch.device("cuda", self.device))
+        rp, _ = _ptr(rank)
+        it = ctypes.c_int32()
+        _check(load().gr_pagerank(self.handle, float(damping), float(tol), int(max_iter), rp, ctypes.byref(it)))
+        return rank, it.value
 
     def sync(self):
         """Wait for the asynchronous runs of this graph; raises on a queue overflow."""

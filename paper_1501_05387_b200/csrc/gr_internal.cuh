@@ -145,6 +145,9 @@ struct Graph {
     // connected components (cc.cu)
     unsigned long long *cc_ctl = nullptr;   // survivors, changed, count
     int2 *cc_list[2] = {nullptr, nullptr};  // edge frontier ping-pong
+    // PageRank (pagerank.cu)
+    double *pr_inv = nullptr, *pr_acc = nullptr;
+    unsigned long long *pr_cnt = nullptr;
 };
 
 gr_status dev_alloc(Graph *g, void **p, size_t bytes);
