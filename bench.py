@@ -65,7 +65,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=16)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2_kron21", choices=sorted(CONFIG_DESC))
-    ap.add_argument("--prim", default="bfs", choices=["bfs", "sssp", "bc"])
+    ap.add_argument("--prim", default="bfs", choices=["bfs", "sssp", "bc", "cc", "pr"])
     ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
     ap.add_argument("--delta", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -434,6 +434,123 @@ def run_bc(args, rank, world, dev):
         dist.destroy_process_group()
 
 
+def run_whole_graph(args, rank, world, dev):
+    """Connected components / PageRank: one step = one full
+    run over the whole graph (gr_cc / gr_pagerank, synchronous: the events
+    include the host reads between passes). GTEPS = m / t for CC and
+    m x iterations / t for PageRank (the paper normalises PageRank to one
+    iteration, Table 3 caption P:1190-1191). Replicas: every rank runs the
+    same whole-graph problem (no data-path collective)."""
+    import torch
+    import torch.distributed as dist
+
+    import graphgen as gg
+    import paper_1501_05387_b200 as gr
+    g = gg.make_config(args.config, device=dev)
+    G = gr.Graph(g.R, g.C, None, symmetric=True)
+    n, m = g.n, g.m
+    comp = torch.empty(n, dtype=torch.int32, device=dev)
+    rank_v = torch.empty(n, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def step():
+        if args.prim == "cc":
+            return 1, G.cc(comp)[1]
+        _, it = G.pagerank(0.85, 1e-6, 1000, rank=rank_v)
+        return it, None
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    l0 = gr.gr_kernel_launch_count()
+    ms, iters = [], []
+    with Clocks(local_index(dev)) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            it, k = step()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+            iters.append(it)
+    launches = gr.gr_kernel_launch_count() - l0
+    tot = sum(ms)
+    if world > 1:
+        t = torch.tensor([tot], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_all = float(t[0])
+    else:
+        tot_all = tot
+    edges = float(m) * sum(iters) * world
+    peak, peak_src = load_peaks()
+    if args.prim == "cc":
+        passes = G.run_stats()["num_levels"]
+        byts = 2 * (8 * n + 4 * m) + (passes + 1) * 8 * n  # lower bound: two CSR passes + jumps + init
+        model = "lower bound: 2 CSR hooking passes (8n + 4m each) + (passes + 1) x 8n (init, pointer jumping)"
+    else:
+        byts = sum(iters) / len(iters) * (40 * n + 4 * m) + 36 * n
+        model = "upper bound per iteration with a full frontier: 40n + 4m (queue, acc, rank, in-list stream); init 36n"
+    achieved = byts / (tot / len(ms) * 1e-3) / 1e9
+    workload = "%s %s" % (args.config, {"cc": "cc (hooking + pointer jumping)",
+                                        "pr": "pagerank (d=0.85, tol=1e-6 per vertex)"}[args.prim])
+    out = {"metric": METRIC, "value": edges / (tot_all * 1e-3) / 1e9, "unit": "GTEPS", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_all / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "int32" if args.prim == "cc" else "f64", "data": "synthetic",
+           "config": {"workload": workload, "graph": CONFIG_DESC[args.config], "n": n, "m": m,
+                      "teps": "m / t" if args.prim == "cc" else "m x iterations / t",
+                      "l2": "flushed (256 MiB write) between timed steps",
+                      "parallelism": "replicas: the whole graph on each of %d rank(s)" % world},
+           "roofline": {"bound": "hbm", "kernel": "cc_hook_*+cc_jump" if args.prim == "cc" else
+                        "pr_advance+pr_filter", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "traffic": None, "peak_source": peak_src, "model": model},
+           "gpu_launches": launches}
+    if args.prim == "pr":
+        out["iterations_per_step"] = sum(iters) / len(iters)
+        out["ms_per_iteration"] = tot_all / sum(iters)
+    if rank == 0:
+        out["clocks"] = clk.summary()
+    # end to end: host (pinned) outputs through the C ABI
+    pin_c = torch.empty(n, dtype=torch.int32, pin_memory=True)
+    pin_r = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    e2e_s, e2e_it = 0.0, 0
+    for _ in range(max(1, min(args.steps, 4))):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        if args.prim == "cc":
+            G.cc(pin_c)
+            e2e_it += 1
+        else:
+            e2e_it += G.pagerank(0.85, 1e-6, 1000, rank=pin_r)[1]
+        e2e_s += time.perf_counter() - t0
+    out["e2e"] = {"value": m * e2e_it / e2e_s / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                  "d2h_bytes_per_step": n * (4 if args.prim == "cc" else 8),
+                  "what": "gr_cc / gr_pagerank through the C ABI writing host (pinned) outputs"}
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        R, C, _ = g.numpy()
+        t0 = time.perf_counter()
+        if args.prim == "cc":
+            oracle.cc(R, C)
+            it = 1
+            what = "one full union-find CC of %s, single-threaded C oracle" % args.config
+        else:
+            oracle.pagerank(R, C, 0.85, tol=1e-6, max_iter=5)
+            it = 5
+            what = "5 Jacobi iterations of the numpy oracle on %s" % args.config
+        cs = time.perf_counter() - t0
+        out["cpu_baseline"] = {"value": m * it / cs / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
+                               "sample": what}
+    if rank == 0:
+        emit(out)
+    G.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def local_index(dev):
     return dev.index if dev.index is not None else 0
 
@@ -463,6 +580,8 @@ def main():
         return run_partitioned(args, rank, world, dev)
     if args.prim == "bc":
         return run_bc(args, rank, world, dev)
+    if args.prim in ("cc", "pr"):
+        return run_whole_graph(args, rank, world, dev)
     want_w = args.prim == "sssp"
     g = gg.make_config(args.config, device=dev, weights=want_w or None)
     G = gr.Graph(g.R, g.C, g.W if want_w else None, symmetric=True)
