@@ -44,6 +44,22 @@ ncu)
      --no-extras > $OUT/ncu_c3_sssp.log 2>&1; echo "ncu c3 sssp rc=$?"
   python scripts/ncu_summary.py $OUT/prof_c3_sssp.ncu-rep $OUT/ncu_c3_sssp_kernel.txt
   ;;
+ncu_more)
+  # one full capture of each session-3 kernel (one launch each; summaries next to them)
+  cap() {  # name, kernel regex, skip, bench args...
+    local name=$1 k=$2 sk=$3; shift 3
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $sk -c 1 \
+       -o $OUT/prof_$name python bench.py --steps 1 --warmup 1 --no-cpu-baseline "$@" > $OUT/ncu_$name.log 2>&1
+    echo "ncu $name rc=$?"
+    python scripts/ncu_summary.py $OUT/prof_$name.ncu-rep $OUT/ncu_${name}.txt
+  }
+  cap c2_bc_fwd bc_fwd_kernel 2 --prim bc
+  cap c2_bc_bwd bc_bwd_kernel 3 --prim bc
+  cap c2_cc_hook cc_hook_csr_kernel 2 --prim cc
+  cap c2_pr_adv pr_advance_kernel 4 --prim pr
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_c2_bc.csv \
+     python bench.py --prim bc --steps 2 --warmup 1 --no-cpu-baseline > $OUT/launches_bc_bench.json 2>&1; echo "launches bc rc=$?"
+  ;;
 esac
 done
 for f in $OUT/bench_*.json; do echo "== $f"; python -c "
