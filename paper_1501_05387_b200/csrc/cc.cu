@@ -44,11 +44,13 @@ struct AllVertexFrontier {
 // Hook one edge: roots a = comp[u], b = comp[v]; if different, the larger
 // root is pointed at the smaller one. Returns true if the edge survives the
 // filter (its endpoints were in different trees when it was read).
-__device__ __forceinline__ bool cc_hook(int32_t *comp, int32_t u, int32_t v) {
-    const int32_t a = __ldcg(comp + u), b = __ldcg(comp + v);
+__device__ __forceinline__ bool cc_hook_ab(int32_t *comp, int32_t a, int32_t b) {
     if (a == b) return false;
     atomicMin(comp + (a > b ? a : b), a > b ? b : a);
     return true;
+}
+__device__ __forceinline__ bool cc_hook(int32_t *comp, int32_t u, int32_t v) {
+    return cc_hook_ab(comp, __ldcg(comp + u), __ldcg(comp + v));
 }
 
 // warp-aggregated append of surviving edges (filter output)
@@ -74,15 +76,20 @@ struct CcHookOp {
     unsigned long long *changed;
     bool half;                   // symmetric graph: each undirected edge once (u < v)
 
-    __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
+    // comp[u] of the list's source, loaded once per window (it may be hooked
+    // during the pass: a stale label is still a vertex of u's tree, and the
+    // edge then survives and is hooked again next pass)
+    __device__ __forceinline__ unsigned long long entry(int32_t v) { return (uint32_t)__ldcg(comp + v); }
 
     template <int U, class T5>
-    __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *,
+    __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *pay,
                                           const int32_t *dst, const T5 *) {
+        int32_t b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) b[u] = (ok[u] && (!half || src[u] < dst[u])) ? __ldcg(comp + dst[u]) : -1;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const bool use = ok[u] && (!half || src[u] < dst[u]);
-            const bool keep = use && cc_hook(comp, src[u], dst[u]);
+            const bool keep = b[u] >= 0 && cc_hook_ab(comp, (int32_t)pay[u], b[u]);
             cc_append(keep, src[u], dst[u], out, cnt, changed);
         }
     }
