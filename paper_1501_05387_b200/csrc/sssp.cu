@@ -69,6 +69,7 @@ struct RelaxOp {
     SsspAppender *farq;
     unsigned long long nimp;
     unsigned long long pol_keep;  // evict_last for dist
+    unsigned long long pol_stream;  // evict_first for the W stream (read once, like C)
 
     __device__ __forceinline__ unsigned long long entry(int32_t v) {
         return ld_probe(dp + v, pol_keep) >> 32;  // dist[u] read when the window is loaded
@@ -83,7 +84,7 @@ struct RelaxOp {
         uint32_t w[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if constexpr (sizeof(T5) == 8) w[u] = ok[u] ? __ldg(W + x[u]) : 0u;
+            if constexpr (sizeof(T5) == 8) w[u] = ok[u] ? ld_stream(W + x[u], pol_stream) : 0u;
             else w[u] = (uint32_t)x[u];
             cur[u] = ok[u] ? ld_probe(dp + dst[u], pol_keep) : 0ull;
         }
@@ -217,7 +218,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             ++it;
             farq.qv = a.far[fp];
             farq.counter = &a.ctl->far_count[fp];
-            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep};
+            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep, policy_evict_first()};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.qr[k & 1], f, mf};
             // same auto rule as BFS (reading A-4): short lists -> thread/warp/CTA
             if (f < a.lb_threshold && mf <= 16 * f && (int64_t)s->ctl[5] <= kTwcMaxDeg)  // no long list (see bfs.cu)

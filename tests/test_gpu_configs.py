@@ -110,3 +110,28 @@ def test_c5_kron25_bfs_certificate(gr):
             _bfs_certificate_torch(g.R, g.C, s, depth, pred)
             depths.append(depth)
         assert torch.equal(depths[0], depths[1])
+
+
+# ---- the paper's other primitives at full size --------
+
+def test_c2_kron21_bc_cc_pagerank(gr):
+    """BC of two sources (fp64, 1e-9 relative), CC (bit-exact labels and
+    count) and PageRank (1e-9 relative after the full-sweep convergence
+    check at tol 1e-12) on the full Kronecker scale-21 graph, in bench.py's
+    launch configuration, against the C / numpy oracle."""
+    g = gg.make_config("c2_kron21", device="cuda")
+    G = gr.Graph(g.R, g.C, None, symmetric=True)
+    R, C, _ = g.numpy()
+    srcs = gg.sources(g, 2)
+    bc = G.bc(srcs).cpu().numpy()
+    ref = oracle.bc(R, C, srcs)
+    nz = ref > 0
+    assert np.array_equal(bc > 0, nz)
+    assert np.max(np.abs(bc[nz] - ref[nz]) / ref[nz]) <= 1e-9
+    comp, k = G.cc()
+    cref, kref = oracle.cc(R, C)
+    assert np.array_equal(comp.cpu().numpy(), cref) and k == kref
+    x, it = G.pagerank(0.85, 1e-12, 1000)
+    xref = oracle.pagerank(R, C, 0.85, tol=1e-15, max_iter=400)
+    assert np.max(np.abs(x.cpu().numpy() - xref) / xref) <= 1e-9, it
+    G.close()
