@@ -287,6 +287,10 @@ struct SmemFrontier {
 //   void edges<U>(ok[], src[], pay[], dst[], eidx[])  process U edges per lane
 // ---------------------------------------------------------------------------
 constexpr int kUnroll = 4;
+#ifndef GR_PF_AHEAD
+#define GR_PF_AHEAD 2
+#endif
+constexpr int kPfAhead = GR_PF_AHEAD;         // uniform groups: L2 prefetch of the C lines this many groups ahead
 constexpr int64_t kMinChunk = 4096;           // dynamic merge-path: min items per piece
 constexpr int64_t kTwcMaxDeg = 4096;          // auto strategy: TWC only without longer lists
 constexpr int kGroup = 32 * kUnroll;          // edges per warp group
@@ -340,7 +344,7 @@ __device__ __forceinline__ void expand_lb_range(const Front &fr, const int32_t *
                 const unsigned long long spv = __shfl_sync(0xffffffffu, pay, kf);
                 const int64_t sh = __shfl_sync(0xffffffffu, shift, kf);
                 // stream ahead: the group after next (4 lines) into L2
-                const int64_t pf = b + 2 * 32 * kUnroll + (int64_t)l * 32;
+                const int64_t pf = b + kPfAhead * 32 * kUnroll + (int64_t)l * 32;
                 if (l < kUnroll && pf < wend) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + pf + sh));
 #pragma unroll
                 for (int u = 0; u < kUnroll; ++u) {
