@@ -55,7 +55,7 @@ __device__ __forceinline__ bool cc_hook(int32_t *comp, int32_t u, int32_t v) {
 
 // warp-aggregated append of surviving edges (filter output)
 __device__ __forceinline__ void cc_append(bool keep, int32_t u, int32_t v, int2 *out, unsigned long long *cnt,
-                                          unsigned long long *changed) {
+                                          unsigned long long *changed, int64_t cap) {
     const unsigned mask = __ballot_sync(0xffffffffu, keep);
     if (!mask) return;
     const int leader = __ffs(mask) - 1;
@@ -66,7 +66,9 @@ __device__ __forceinline__ void cc_append(bool keep, int32_t u, int32_t v, int2 
     }
     if (!out) return;
     base = __shfl_sync(0xffffffffu, base, leader);
-    if (keep) out[base + __popc(mask & lanemask_lt())] = make_int2(u, v);
+    const unsigned long long pos = base + __popc(mask & lanemask_lt());
+    if (keep && pos < (unsigned long long)cap) out[pos] = make_int2(u, v);
+    else if (keep) changed[2] = 1ull;  // list overflow: a GR_SYMMETRIC graph that is not symmetric
 }
 
 struct CcHookOp {
@@ -75,6 +77,7 @@ struct CcHookOp {
     unsigned long long *cnt;
     unsigned long long *changed;
     bool half;                   // symmetric graph: each undirected edge once (u < v)
+    int64_t cap;                 // edge-list capacity
 
     // comp[u] of the list's source, loaded once per window (it may be hooked
     // during the pass: a stale label is still a vertex of u's tree, and the
@@ -90,7 +93,7 @@ struct CcHookOp {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const bool keep = b[u] >= 0 && cc_hook_ab(comp, (int32_t)pay[u], b[u]);
-            cc_append(keep, src[u], dst[u], out, cnt, changed);
+            cc_append(keep, src[u], dst[u], out, cnt, changed, cap);
         }
     }
 };
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(kCcBlock) cc_hook_csr_kernel(const int64_t *R,
 
 __global__ void __launch_bounds__(kCcBlock) cc_hook_list_kernel(int32_t *comp, const int2 *in, int64_t k, int2 *out,
                                                                 unsigned long long *cnt,
-                                                                unsigned long long *changed) {
+                                                                unsigned long long *changed, int64_t cap) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t base = tid - lane_id(); base < k; base += nt) {  // warp-uniform trip count
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(kCcBlock) cc_hook_list_kernel(int32_t *comp, c
             e = __ldcs(in + j);
             keep = cc_hook(comp, e.x, e.y);
         }
-        cc_append(keep, e.x, e.y, out, cnt, changed);
+        cc_append(keep, e.x, e.y, out, cnt, changed, cap);
     }
 }
 
@@ -186,6 +189,7 @@ gr_status gr_cc(gr_graph *h, int32_t *comp_out, int64_t *num_components) {
     int cur = 0, passes = 0;
     for (;;) {
         GR_CUDA(cudaMemsetAsync(g->cc_ctl, 0, 2 * sizeof(unsigned long long), s));
+        if (passes == 0) GR_CUDA(cudaMemsetAsync(g->cc_ctl + 3, 0, sizeof(unsigned long long), s));
         if (k < 0) {
             // CSR passes: the first hooks only; the second also writes the survivors
             int2 *out = nullptr;
@@ -199,18 +203,22 @@ gr_status gr_cc(gr_graph *h, int32_t *comp_out, int64_t *num_components) {
                 list[1] = g->cc_list[1];
                 out = list[cur];
             }
-            CcHookOp op{comp, out, cnt, changed, half};
+            CcHookOp op{comp, out, cnt, changed, half, cap};
             cc_hook_csr_kernel<<<grid, kCcBlock, 0, s>>>(g->R, g->C, n, m, op);
         } else {
-            cc_hook_list_kernel<<<grid, kCcBlock, 0, s>>>(comp, list[cur], k, list[cur ^ 1], cnt, changed);
+            cc_hook_list_kernel<<<grid, kCcBlock, 0, s>>>(comp, list[cur], k, list[cur ^ 1], cnt, changed, cap);
             cur ^= 1;
         }
         cc_jump_kernel<<<g->num_sms * 8, 256, 0, s>>>(comp, n);
         launches += 2;
-        unsigned long long hc[2] = {0, 0};
+        unsigned long long hc[4] = {0, 0, 0, 0};
         GR_CUDA(cudaMemcpyAsync(hc, g->cc_ctl, sizeof(hc), cudaMemcpyDeviceToHost, s));
         GR_CUDA(cudaStreamSynchronize(s));
         ++passes;
+        if (hc[3]) {
+            set_error("edge frontier overflow: the graph was created GR_SYMMETRIC but is not symmetric");
+            return GR_ERR_INVALID_GRAPH;
+        }
         if (!hc[1]) break;                 // no edge crossed two trees: converged
         if (passes >= 2) k = (int64_t)hc[0];
         if (k == 0) break;

@@ -290,7 +290,10 @@ constexpr int kUnroll = 4;
 #ifndef GR_PF_AHEAD
 #define GR_PF_AHEAD 2
 #endif
-constexpr int kPfAhead = GR_PF_AHEAD;         // uniform groups: L2 prefetch of the C lines this many groups ahead
+constexpr int kPfAhead = GR_PF_AHEAD;
+#ifndef GR_PIPE2
+#define GR_PIPE2 0
+#endif         // uniform groups: L2 prefetch of the C lines this many groups ahead
 constexpr int64_t kMinChunk = 4096;           // dynamic merge-path: min items per piece
 constexpr int64_t kTwcMaxDeg = 4096;          // auto strategy: TWC only without longer lists
 constexpr int kGroup = 32 * kUnroll;          // edges per warp group
@@ -326,7 +329,10 @@ __device__ __forceinline__ void expand_lb_range(const Front &fr, const int32_t *
         int64_t wend = __shfl_sync(0xffffffffu, end, 31);
         GR_TSTAMP(2);
         if (wend > e1) wend = e1;
-        for (int64_t b = e; b < wend; b += 32 * kUnroll) {
+        // one group = 32 x kUnroll consecutive edges of the window: owner
+        // search (uniform fast path or 5-step shuffle search) + C loads
+        auto group = [&](int64_t b, bool *ok, int32_t *src, unsigned long long *sp, int64_t *eidx,
+                         int32_t *dst) {
             // offsets relative to the batch start fit in 32 bits (clamped)
             const int64_t rel64 = o - b;
             const int32_t rel = rel64 < -0x7fffffffLL ? -0x7fffffff : (rel64 > 0x7fffffffLL ? 0x7fffffff : (int32_t)rel64);
@@ -334,16 +340,11 @@ __device__ __forceinline__ void expand_lb_range(const Front &fr, const int32_t *
             const unsigned first = __ballot_sync(0xffffffffu, rel <= 0);
             const unsigned last = __ballot_sync(0xffffffffu, rel <= 32 * kUnroll - 1);
             const int kf = 31 - __clz(first), kl = 31 - __clz(last);
-            bool ok[kUnroll];
-            int32_t src[kUnroll];
-            unsigned long long sp[kUnroll];
-            int64_t eidx[kUnroll];
-            int32_t dst[kUnroll];
             if (kf == kl) {
                 const int32_t sv = __shfl_sync(0xffffffffu, v, kf);
                 const unsigned long long spv = __shfl_sync(0xffffffffu, pay, kf);
                 const int64_t sh = __shfl_sync(0xffffffffu, shift, kf);
-                // stream ahead: the group after next (4 lines) into L2
+                // stream ahead: a later group (4 lines) into L2
                 const int64_t pf = b + kPfAhead * 32 * kUnroll + (int64_t)l * 32;
                 if (l < kUnroll && pf < wend) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + pf + sh));
 #pragma unroll
@@ -373,10 +374,47 @@ __device__ __forceinline__ void expand_lb_range(const Front &fr, const int32_t *
             }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) dst[u] = ok[u] ? ld_stream(C + eidx[u], pol) : 0;
+        };
+#if GR_PIPE2
+        // two groups in flight: the C loads of group g+1 are issued before
+        // group g's per-edge work (probes, claims, appends) starts
+        bool ok[kUnroll];
+        int32_t src[kUnroll];
+        unsigned long long sp[kUnroll];
+        int64_t eidx[kUnroll];
+        int32_t dst[kUnroll];
+        if (e < wend) group(e, ok, src, sp, eidx, dst);
+        for (int64_t b = e; b < wend; b += 32 * kUnroll) {
+            bool ok1[kUnroll];
+            int32_t src1[kUnroll];
+            unsigned long long sp1[kUnroll];
+            int64_t eidx1[kUnroll];
+            int32_t dst1[kUnroll];
+            const bool more = b + 32 * kUnroll < wend;
+            if (more) group(b + 32 * kUnroll, ok1, src1, sp1, eidx1, dst1);
+            GR_TSTAMP(3);
+            op.template edges<kUnroll>(ok, src, sp, dst, eidx);
+            GR_TSTAMP(4);
+            if (more) {
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    ok[u] = ok1[u]; src[u] = src1[u]; sp[u] = sp1[u]; eidx[u] = eidx1[u]; dst[u] = dst1[u];
+                }
+            }
+        }
+#else
+        for (int64_t b = e; b < wend; b += 32 * kUnroll) {
+            bool ok[kUnroll];
+            int32_t src[kUnroll];
+            unsigned long long sp[kUnroll];
+            int64_t eidx[kUnroll];
+            int32_t dst[kUnroll];
+            group(b, ok, src, sp, eidx, dst);
             GR_TSTAMP(3);
             op.template edges<kUnroll>(ok, src, sp, dst, eidx);
             GR_TSTAMP(4);
         }
+#endif
         e = wend;
         i += 32;
     }
