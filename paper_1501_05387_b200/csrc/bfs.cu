@@ -500,7 +500,10 @@ __device__ __forceinline__ long long gtimer() {
 template <int kBlk>
 __host__ __device__ constexpr size_t bfs_sbm_offset() { return (sizeof(BfsSmemT<kBlk / kWarp>) + 127) & ~(size_t)127; }
 
-template <int kBlk, int kMinB>
+// kPush: direction forced to push (gr_bfs_opts.direction = 1): the pull and
+// bitmap-conversion paths are compiled out, which frees registers for the
+// push advance (fewer spills at the 64-register cap).
+template <int kBlk, int kMinB, bool kPush = false>
 __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
     constexpr int kNW = kBlk / kWarp;
     using BfsSmem = BfsSmemT<kNW>;
@@ -608,7 +611,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
         const bool stop = (f == 0 || s->ctl[3]);
         __syncthreads();  // s->ctl is rewritten below
         if (stop) break;
-        const int dir = decide_direction(a, st.dir, f, mf, st.u_cnt, st.m_u, st.prev_f, nwords);
+        const int dir = kPush ? 1 : decide_direction(a, st.dir, f, mf, st.u_cnt, st.m_u, st.prev_f, nwords);
         if (dir == 1 && !st.q_valid) {
             // the frontier of the last pull step exists as a bitmap only
             Appender conv = app;
@@ -646,7 +649,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
                     GR_TSTAMP(0);
                     if (mu_pending) { st.m_u -= E; mu_pending = false; }
                     if (cf == 0) { done = true; break; }
-                    const int d = decide_direction(a, st.dir, cf, E, st.u_cnt, st.m_u, st.prev_f, nwords);
+                    const int d = kPush ? 1 : decide_direction(a, st.dir, cf, E, st.u_cnt, st.m_u, st.prev_f, nwords);
                     if (!(d == 1 && E <= a.small_e)) break;
                     st.dir = d;
                     const int Lc = st.L;
@@ -921,7 +924,10 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     const bool use_snap = env_int("GR_SNAPSHOT", 0) != 0 && nwords * 4 > env_int("GR_SNAP_MIN_BYTES", 64 << 10);
     static int optin = 0;
     if (optin == 0) GR_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
-    const void *fn = use_snap ? (const void *)bfs_kernel<1024, 1> : (const void *)bfs_kernel<kBlock, kMinBlocks>;
+    const bool push_only = a.direction == 1 && !use_snap && env_int("GR_PUSH_KERNEL", 0) != 0;  // measured 3% slower: off
+    const void *fn = use_snap ? (const void *)bfs_kernel<1024, 1>
+                   : push_only ? (const void *)bfs_kernel<kBlock, kMinBlocks, true>
+                               : (const void *)bfs_kernel<kBlock, kMinBlocks>;
     const int block = use_snap ? 1024 : kBlock;
     size_t smem;
     a.sbm_words = 0;
@@ -935,10 +941,11 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     } else {
         smem = sizeof(BfsSmemT<kBlock / kWarp>);
     }
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[use_snap]) {
+    static bool attr_set[3] = {false, false, false};
+    const int variant = use_snap ? 1 : push_only ? 2 : 0;
+    if (!attr_set[variant]) {
         GR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
-        attr_set[use_snap] = true;
+        attr_set[variant] = true;
     }
     int per_sm = 0;
     GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
