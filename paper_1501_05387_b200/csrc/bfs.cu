@@ -951,7 +951,10 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, block, smem));
     if (per_sm < 1) { set_error("bfs_kernel cannot be resident"); return GR_ERR_CUDA; }
     if (per_sm > (use_snap ? 1 : kMinBlocks)) per_sm = use_snap ? 1 : kMinBlocks;
-    dim3 grid(g->num_sms * per_sm), blk(block);
+    int64_t ctas = (int64_t)g->num_sms * per_sm;
+    const int64_t cap_ctas = env_int("GR_BFS_CTAS", 0);  // experiment: fewer persistent CTAs
+    if (cap_ctas > 0 && cap_ctas < ctas) ctas = cap_ctas;
+    dim3 grid((unsigned)ctas), blk(block);
     void *args[] = {&a};
     GR_CUDA(cudaLaunchCooperativeKernel(fn, grid, blk, args, smem, g->stream));
     count_launch();

@@ -334,7 +334,10 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
         GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sssp_kernel, kBlock, smem));
     }
     if (per_sm < 1) { set_error("sssp_kernel cannot be resident"); return GR_ERR_CUDA; }
-    dim3 grid(g->num_sms * per_sm), block(kBlock);
+    int64_t ctas = (int64_t)g->num_sms * per_sm;
+    const int64_t cap_ctas = env_int("GR_SSSP_CTAS", 0);  // experiment: fewer persistent CTAs
+    if (cap_ctas > 0 && cap_ctas < ctas) ctas = cap_ctas;
+    dim3 grid((unsigned)ctas), block(kBlock);
     void *args[] = {&a};
     GR_CUDA(cudaLaunchCooperativeKernel((void *)sssp_kernel, grid, block, args, smem, g->stream));
     unpack_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->dp, g->n, dist, pred);
