@@ -38,12 +38,22 @@ constexpr int kBcWarps = kBcBlock / 32;
 constexpr int kBcStage = 64;
 using BcAppender = AppenderT<kBcStage>;
 
+// Per-vertex BC state in ONE 16-byte record, so the random per-edge accesses
+// of both passes touch one 32-B sector: depth (probe + CAS claim) and sigma
+// (atomicAdd) in the forward pass; depth and coef = (1 + delta) / sigma of
+// the successor in the backward pass (val holds sigma until the vertex's
+// level has been processed backwards, then coef).
+struct __align__(16) BcVert {
+    double val;
+    int32_t depth;
+    int32_t pad;
+};
+
 struct BcArgs {
     int64_t n;
     const int64_t *R;
     const int32_t *C;
-    int32_t *depth;
-    double *sigma;
+    BcVert *bv;
     double *delta;
     int32_t *qv;               // all levels back to back
     int64_t *qo;
@@ -58,7 +68,7 @@ struct BcFwdOp {
     BcAppender *app;
 
     __device__ __forceinline__ unsigned long long entry(int32_t v) {
-        return (unsigned long long)__double_as_longlong(__ldcg(a->sigma + v));
+        return (unsigned long long)__double_as_longlong(__ldcg(&a->bv[v].val));
     }
 
     template <int U, class T5>
@@ -66,7 +76,7 @@ struct BcFwdOp {
                                           const int32_t *dst, const T5 *) {
         int32_t d[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) d[u] = ok[u] ? __ldcg(a->depth + dst[u]) : -2;
+        for (int u = 0; u < U; ++u) d[u] = ok[u] ? __ldcg(&a->bv[dst[u]].depth) : -2;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t w = dst[u];
@@ -74,13 +84,15 @@ struct BcFwdOp {
             int64_t deg = 0, rs = 0;
             int32_t dw = d[u];
             if (dw == -1) {
-                dw = atomicCAS(a->depth + w, -1, next);
+                dw = atomicCAS(&a->bv[w].depth, -1, next);
                 disc = dw == -1;
                 if (disc) dw = next;
             }
-            if (dw == next) atomicAdd(a->sigma + w, __longlong_as_double((long long)pay[u]));
+            if (dw == next) atomicAdd(&a->bv[w].val, __longlong_as_double((long long)pay[u]));
             if (disc) { rs = a->R[w]; deg = a->R[w + 1] - rs; }
-            app->push(disc && deg > 0, w, deg, rs);
+            // every discovered vertex joins its level's queue (degree 0 too:
+            // the backward pass converts its sigma into coef)
+            app->push(disc, w, deg, rs);
         }
     }
 };
@@ -90,22 +102,22 @@ struct BcBwdOp {
     int32_t next;              // L + 1
 
     __device__ __forceinline__ unsigned long long entry(int32_t v) {
-        return (unsigned long long)__double_as_longlong(__ldcg(a->sigma + v));
+        return (unsigned long long)__double_as_longlong(__ldcg(&a->bv[v].val));  // sigma[v]
     }
 
     template <int U, class T5>
     __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *pay,
                                           const int32_t *dst, const T5 *) {
-        int32_t d[U];
+        double2 r[U];  // {val, (depth, pad)} of the successor candidate: one 16-B load
 #pragma unroll
-        for (int u = 0; u < U; ++u) d[u] = ok[u] ? __ldcg(a->depth + dst[u]) : -2;
+        for (int u = 0; u < U; ++u) r[u] = ok[u] ? __ldcg(reinterpret_cast<const double2 *>(a->bv + dst[u]))
+                                                 : make_double2(0.0, 0.0);
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             double c = 0.0;
-            if (d[u] == next) {  // w is a successor of v on a shortest path
-                const int32_t w = dst[u];
-                c = __longlong_as_double((long long)pay[u]) / __ldcg(a->sigma + w) * (1.0 + __ldcg(a->delta + w));
-            }
+            const int32_t dw = ok[u] ? (int32_t)(__double_as_longlong(r[u].y) & 0xffffffffll) : -2;
+            if (dw == next)  // w is a successor of v: sigma[v] * (1 + delta[w]) / sigma[w]
+                c = __longlong_as_double((long long)pay[u]) * r[u].x;
             const int32_t s0 = __shfl_sync(0xffffffffu, src[u], 0);
             if (__all_sync(0xffffffffu, src[u] == s0)) {
                 c = warp_sum<double>(c);
@@ -121,8 +133,11 @@ __global__ void bc_init_kernel(BcArgs a, int32_t s) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t v = tid; v < a.n; v += nt) {
-        a.depth[v] = v == s ? 0 : -1;
-        a.sigma[v] = v == s ? 1.0 : 0.0;
+        BcVert x;
+        x.val = v == s ? 1.0 : 0.0;   // sigma
+        x.depth = v == s ? 0 : -1;
+        x.pad = 0;
+        a.bv[v] = x;
         a.delta[v] = 0.0;
     }
     if (tid == 0) {
@@ -130,9 +145,25 @@ __global__ void bc_init_kernel(BcArgs a, int32_t s) {
         a.qv[0] = s;
         a.qo[0] = 0;
         a.qr[0] = a.R[s];
-        a.cnt[0] = d > 0 ? (((unsigned long long)d << a.S) | 1ull) : 0ull;
+        a.cnt[0] = ((unsigned long long)d << a.S) | 1ull;
         a.cnt[1] = 0ull;
     }
+}
+
+// level L processed backwards: val = sigma -> coef = (1 + delta) / sigma
+__global__ void bc_coef_kernel(BcArgs a, int64_t off, int64_t f) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t j = tid; j < f; j += nt) {
+        const int32_t v = a.qv[off + j];
+        a.bv[v].val = (1.0 + a.delta[v]) / a.bv[v].val;
+    }
+}
+
+__global__ void bc_sigma_kernel(const BcVert *bv, int64_t n, double *sigma) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < n; v += nt) sigma[v] = bv[v].depth >= 0 ? bv[v].val : 0.0;
 }
 
 __global__ void __launch_bounds__(kBcBlock) bc_fwd_kernel(BcArgs a, int L, int64_t off, int64_t f, int64_t mf) {
@@ -201,9 +232,8 @@ gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_ou
     if (g->pending && gr_graph_sync(h) != GR_OK) return GR_ERR_OVERFLOW;
     gr_status st;
     const int64_t n = g->n;
-    if (!g->bc_sigma) {
-        if ((st = dev_alloc(g, (void **)&g->bc_depth, n * sizeof(int32_t))) != GR_OK ||
-            (st = dev_alloc(g, (void **)&g->bc_sigma, n * sizeof(double))) != GR_OK ||
+    if (!g->bc_vert) {
+        if ((st = dev_alloc(g, &g->bc_vert, n * sizeof(BcVert))) != GR_OK ||
             (st = dev_alloc(g, (void **)&g->bc_delta, n * sizeof(double))) != GR_OK ||
             (st = dev_alloc(g, (void **)&g->bc_cnt, (n + 3) * sizeof(unsigned long long))) != GR_OK)
             return st;
@@ -216,7 +246,15 @@ gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_ou
     }
     BcArgs a;
     a.n = n; a.R = g->R; a.C = g->C;
-    a.depth = g->bc_depth; a.sigma = g->bc_sigma; a.delta = g->bc_delta;
+    a.bv = (BcVert *)g->bc_vert; a.delta = g->bc_delta;
+    double *sig = nullptr;  // sigma of the last source, saved before the backward pass overwrites it
+    if (sigma_out && nsrc > 0) {
+        if (ptr_on_device(sigma_out)) sig = sigma_out;
+        else {
+            if (!g->bc_sig && (st = dev_alloc(g, (void **)&g->bc_sig, n * sizeof(double))) != GR_OK) return st;
+            sig = g->bc_sig;
+        }
+    }
     a.qv = g->qv[0]; a.qo = g->qo[0]; a.qr = g->qr[0];
     a.cnt = g->bc_cnt; a.S = g->pack_shift;
     const int grid = g->num_sms * 8;
@@ -245,18 +283,29 @@ gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_ou
             off.push_back(off[L] + f);
         }
         levels_total += (int)fs.size();
-        // backward phase: the stored frontiers, deepest first (level 0 = the
-        // source, whose delta is not accumulated but is cheap to compute)
-        for (int L = (int)fs.size() - 1; L >= 1; --L) {
-            bc_bwd_kernel<<<grid, kBcBlock, 0, s>>>(a, L, off[L], fs[L], mfs[L]);
+        if (sig && i == nsrc - 1) {
+            bc_sigma_kernel<<<g->num_sms * 4, 256, 0, s>>>(a.bv, n, sig);
             ++launches;
+        }
+        // backward phase: the stored frontiers, deepest first (the deepest
+        // level has no successors: only its coef; level 0 = the source, whose
+        // dependency is not accumulated)
+        for (int L = (int)fs.size() - 1; L >= 1; --L) {
+            if (L + 1 < (int)fs.size()) {
+                bc_bwd_kernel<<<grid, kBcBlock, 0, s>>>(a, L, off[L], fs[L], mfs[L]);
+                ++launches;
+            }
+            if (L > 1) {  // coef of level L is read by level L - 1 >= 1 only
+                bc_coef_kernel<<<g->num_sms * 2, 256, 0, s>>>(a, off[L], fs[L]);
+                ++launches;
+            }
         }
         bc_accum_kernel<<<g->num_sms * 4, 256, 0, s>>>(a.delta, n, src, bc);
         ++launches;
     }
     GR_CUDA(cudaGetLastError());
     if (!dev_bc) GR_CUDA(cudaMemcpyAsync(bc_out, bc, n * sizeof(double), cudaMemcpyDeviceToHost, s));
-    if (sigma_out && nsrc > 0) GR_CUDA(cudaMemcpyAsync(sigma_out, a.sigma, n * sizeof(double), cudaMemcpyDefault, s));
+    if (sig && sig != sigma_out) GR_CUDA(cudaMemcpyAsync(sigma_out, sig, n * sizeof(double), cudaMemcpyDeviceToHost, s));
     GR_CUDA(cudaStreamSynchronize(s));
     count_launch(launches);
     g->last_launches = launches;

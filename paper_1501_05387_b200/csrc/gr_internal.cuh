@@ -139,8 +139,8 @@ struct Graph {
     uint32_t *ps_dist = nullptr;            // caller's outputs (gr_part_sssp_begin)
     int32_t *ps_pred = nullptr;
     // betweenness centrality (bc.cu)
-    int32_t *bc_depth = nullptr;
-    double *bc_sigma = nullptr, *bc_delta = nullptr, *bc_buf = nullptr;
+    void *bc_vert = nullptr;                // [n] 16-B (sigma|coef, depth) records (bc.cu BcVert)
+    double *bc_sig = nullptr, *bc_delta = nullptr, *bc_buf = nullptr;
     unsigned long long *bc_cnt = nullptr;   // [n + 3] per-level packed counters
     // connected components (cc.cu)
     unsigned long long *cc_ctl = nullptr;   // survivors, changed, count
