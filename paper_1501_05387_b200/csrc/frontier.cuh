@@ -67,6 +67,7 @@ struct AppenderT {
     int64_t cap;                    // queue capacity
     unsigned long long *overflow;
     unsigned long long *dmax = nullptr;  // max appended degree (offsets mode; null: not tracked)
+    bool stream = false;            // streaming (evict-first) queue stores: keep L2 for per-vertex state
 
     __device__ __forceinline__ void flush() {
         const unsigned l = lane_id();
@@ -108,12 +109,20 @@ struct AppenderT {
                     const int64_t d = (j < k) ? (int64_t)sd[j] : 0;
                     const int64_t x = warp_incl_scan<int64_t>(d);
                     if (j < k) {
-                        qo[cbase + j] = run + x - d;
-                        qr[cbase + j] = sr[j];
+                        if (stream) {
+                            __stcs(qo + cbase + j, run + x - d);
+                            __stcs(qr + cbase + j, sr[j]);
+                        } else {
+                            qo[cbase + j] = run + x - d;
+                            qr[cbase + j] = sr[j];
+                        }
                     }
                     run += __shfl_sync(0xffffffffu, x, 31);
                 }
-                if (j < k) qv[cbase + j] = sv[j];
+                if (j < k) {
+                    if (stream) __stcs(qv + cbase + j, sv[j]);
+                    else qv[cbase + j] = sv[j];
+                }
             }
         }
         __syncwarp();

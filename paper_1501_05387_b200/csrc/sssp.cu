@@ -31,6 +31,7 @@ struct SsspArgs {
     int32_t src;
     uint64_t delta;
     int64_t lb_threshold;     // auto strategy: thread/warp/CTA only below this frontier size (A-4)
+    int stream_queues;        // near/far queue stores with the streaming cache hint
     int S;
 };
 
@@ -120,6 +121,7 @@ __device__ __forceinline__ long long sssp_gtimer() {
 }
 
 __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
+    const bool env_stream = a.stream_queues;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SsspSmem *s = reinterpret_cast<SsspSmem *>(smem_raw);
@@ -162,6 +164,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
     nearq.cap = a.n;
     nearq.overflow = &a.ctl->overflow;
     farq.sv = s->fv[wib]; farq.sd = nullptr; farq.cnt = 0; farq.qo = nullptr; farq.S = 0;
+    nearq.stream = farq.stream = env_stream;
     farq.cap = a.far_cap; farq.overflow = &a.ctl->overflow;
     const unsigned long long pol_keep = policy_evict_last();
 
@@ -326,6 +329,7 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.src = src;
     a.delta = delta;
     a.lb_threshold = env_int("GR_SSSP_LB_THRESHOLD", 65536);
+    a.stream_queues = (int)env_int("GR_SSSP_STREAMQ", 0);
     a.S = g->pack_shift;
     static int per_sm = 0;
     const size_t smem = sizeof(SsspSmem);
