@@ -1,7 +1,8 @@
 """compute-sanitizer over every kernel path on small graphs:
 memcheck (out-of-bounds / misaligned), racecheck (shared-memory hazards),
 synccheck (barrier misuse). scripts/sanitize.py runs BFS in every direction x
-strategy and SSSP on symmetric and directed graphs and checks the oracle."""
+strategy, SSSP, BC, CC and PageRank on symmetric and directed graphs, and the
+partitioned BFS / SSSP kernels (3 loopback partitions), and checks the oracle."""
 import os
 import shutil
 import subprocess
