@@ -15,7 +15,8 @@
 // reading it.
 // B200 design: the advance runs over IN-lists (CSC; the CSR itself for
 // symmetric graphs) of the frontier vertices with the merge-path balancer;
-// per edge the contribution PR(u) * inv_outdeg(u) is summed into acc[v] -- a
+// per edge the contribution y[u] = PR(u) / outdeg(u) (kept per vertex by the
+// filter, so one random 8-B load per edge) is summed into acc[v] -- a
 // warp whose 32 edges share v reduces in registers and issues one fp64
 // atomicAdd (the paper's AtomicAdd, aggregated). The filter kernel turns acc
 // into the new rank (Jacobi within an iteration: all reads of a step happen
@@ -33,8 +34,7 @@ constexpr int kPrStage = 64;
 using PrAppender = AppenderT<kPrStage>;
 
 struct PrAccOp {
-    const double *x;
-    const double *inv;    // 1 / outdeg(u) (0 for dangling u)
+    const double *y;      // y[u] = PR(u) / outdeg(u) (0 for dangling u), kept by the filter
     double *acc;
 
     __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
@@ -44,7 +44,7 @@ struct PrAccOp {
                                           const int32_t *dst, const T5 *) {
         double c[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) c[u] = ok[u] ? __ldg(x + dst[u]) * __ldg(inv + dst[u]) : 0.0;
+        for (int u = 0; u < U; ++u) c[u] = ok[u] ? __ldg(y + dst[u]) : 0.0;  // one random sector per edge
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t s0 = __shfl_sync(0xffffffffu, src[u], 0);
@@ -58,7 +58,8 @@ struct PrAccOp {
     }
 };
 
-__global__ void pr_init_kernel(const int64_t *R, const int64_t *Rt, int64_t n, double *x, double *inv, double *acc,
+__global__ void pr_init_kernel(const int64_t *R, const int64_t *Rt, int64_t n, double *x, double *inv, double *y,
+                               double *acc,
                                int32_t *qv, int64_t *qr, int64_t *qo, unsigned long long *cnt, int S) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t nt = (int64_t)gridDim.x * blockDim.x;
@@ -66,6 +67,7 @@ __global__ void pr_init_kernel(const int64_t *R, const int64_t *Rt, int64_t n, d
         const int64_t od = R[v + 1] - R[v];
         x[v] = 1.0 / (double)n;
         inv[v] = od > 0 ? 1.0 / (double)od : 0.0;
+        y[v] = x[v] * inv[v];
         acc[v] = 0.0;
         qv[v] = (int32_t)v;        // frontier 0 = every vertex, in-list prefix = Rt
         qr[v] = Rt[v];
@@ -98,8 +100,8 @@ __global__ void pr_refill_kernel(const int64_t *Rt, int64_t n, int32_t *qv, int6
 
 // filter: new rank, converged vertices leave the frontier
 __global__ void __launch_bounds__(kPrBlock) pr_filter_kernel(const int64_t *Rt, const int32_t *qv, int64_t f,
-                                                             double *x, double *acc, double base, double d,
-                                                             double tol, PrAppender app) {
+                                                             double *x, const double *inv, double *y, double *acc,
+                                                             double base, double d, double tol, PrAppender app) {
     __shared__ int32_t s_v[kPrWarps][kPrStage];
     __shared__ int32_t s_d[kPrWarps][kPrStage];
     __shared__ int64_t s_r[kPrWarps][kPrStage];
@@ -118,6 +120,7 @@ __global__ void __launch_bounds__(kPrBlock) pr_filter_kernel(const int64_t *Rt, 
             acc[v] = 0.0;
             keep = fabs(xn - x[v]) > tol * xn;
             x[v] = xn;
+            y[v] = xn * inv[v];
             if (keep) { rs = Rt[v]; deg = Rt[v + 1] - rs; }
         }
         app.push(keep, v, deg, rs);
@@ -145,7 +148,7 @@ gr_status gr_pagerank(gr_graph *h, double damping, double tol, int32_t max_iter,
     gr_status st;
     const int64_t n = g->n;
     if (!g->pr_inv) {
-        if ((st = dev_alloc(g, (void **)&g->pr_inv, n * sizeof(double))) != GR_OK ||
+        if ((st = dev_alloc(g, (void **)&g->pr_inv, 2 * n * sizeof(double))) != GR_OK ||  // inv | y
             (st = dev_alloc(g, (void **)&g->pr_acc, n * sizeof(double))) != GR_OK ||
             (st = dev_alloc(g, (void **)&g->pr_cnt, 4 * sizeof(unsigned long long))) != GR_OK)
             return st;
@@ -158,7 +161,8 @@ gr_status gr_pagerank(gr_graph *h, double damping, double tol, int32_t max_iter,
     }
     cudaStream_t s = g->stream;
     const int S = g->pack_shift;
-    pr_init_kernel<<<g->num_sms * 4, 256, 0, s>>>(g->R, g->Rt, n, x, g->pr_inv, g->pr_acc, g->qv[0], g->qr[0],
+    double *inv = g->pr_inv, *y = g->pr_inv + n;
+    pr_init_kernel<<<g->num_sms * 4, 256, 0, s>>>(g->R, g->Rt, n, x, inv, y, g->pr_acc, g->qv[0], g->qr[0],
                                                    g->qo[0], g->pr_cnt, S);
     int launches = 1, it = 0;
     const double base = (1.0 - damping) / (double)n;
@@ -184,7 +188,7 @@ gr_status gr_pagerank(gr_graph *h, double damping, double tol, int32_t max_iter,
             full = full && it == 0;
         }
         const int c = it & 1;
-        PrAccOp op{x, g->pr_inv, g->pr_acc};
+        PrAccOp op{y, g->pr_acc};
         if (mf > 0)
             pr_advance_kernel<<<g->num_sms * 8, kPrBlock, 0, s>>>(g->Ct, g->qv[c], g->qo[c], g->qr[c], f, mf, op);
         GR_CUDA(cudaMemsetAsync(g->pr_cnt + (c ^ 1), 0, sizeof(unsigned long long), s));
@@ -195,7 +199,7 @@ gr_status gr_pagerank(gr_graph *h, double damping, double tol, int32_t max_iter,
         app.counter = g->pr_cnt + (c ^ 1);
         const int64_t blocks = (f + kPrBlock - 1) / kPrBlock;
         pr_filter_kernel<<<(int)(blocks < g->num_sms * 8 ? blocks : g->num_sms * 8), kPrBlock, 0, s>>>(
-            g->Rt, g->qv[c], f, x, g->pr_acc, base, damping, tol, app);
+            g->Rt, g->qv[c], f, x, inv, y, g->pr_acc, base, damping, tol, app);
         launches += 2;
     }
     if (!dev_out) GR_CUDA(cudaMemcpyAsync(rank_out, x, n * sizeof(double), cudaMemcpyDeviceToHost, s));
