@@ -317,6 +317,14 @@ gr_status gr_part_bfs_absorb(gr_graph *g, int32_t level, const int32_t *recv_pai
 /* Local frontier of level `level` (after expand+absorb of level-1): vertex
  * count and edge count (host outputs). */
 gr_status gr_part_bfs_frontier(gr_graph *g, int32_t level, int64_t *f, int64_t *mf);
+/* As gr_part_bfs_frontier, without a host synchronisation: enqueues on the
+ * graph's stream a write of {f, m_f, overflow} to DEVICE int64 out3[3]
+ * (overflow: 0 none, 1 local queue overflow, 2 a received vertex this rank
+ * does not own). The caller sums out3 over ranks on the device (one NCCL
+ * all-reduce) and reads the totals once per level; overflow != 0 must be
+ * treated as the GR_ERR_OVERFLOW gr_part_bfs_frontier would return. Host
+ * out3 is rejected with GR_ERR_INVALID_ARGUMENT. */
+gr_status gr_part_bfs_frontier_async(gr_graph *g, int32_t level, int64_t *out3);
 
 /* Dense (pull) levels of a partitioned BFS, for
  * symmetric graphs (out-lists double as in-lists):

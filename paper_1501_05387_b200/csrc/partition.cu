@@ -283,6 +283,17 @@ static PartArgs part_args(Graph *g) {
 
 using namespace gr;
 
+// Device-side frontier readout (no host synchronisation): out[0] = f,
+// out[1] = m_f of level `level`, out[2] = overflow code (0 none, 1 queue, 2
+// misrouted pair). The caller sums out[] over ranks on the device and reads
+// the totals once per level.
+__global__ void part_frontier_kernel(const Ctl *ctl, int level, int S, long long *out) {
+    const unsigned long long qp = ctl->slot[level & 3].qpack;
+    out[0] = (long long)(qp & ((1ull << S) - 1));
+    out[1] = (long long)(qp >> S);
+    out[2] = (long long)ctl->overflow;
+}
+
 extern "C" {
 
 static gr_status create_part(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin, int64_t v_end,
@@ -431,6 +442,18 @@ gr_status gr_part_bfs_frontier(gr_graph *h, int32_t level, int64_t *f, int64_t *
     }
     if (f) *f = (int64_t)(qp & ((1ull << g->pack_shift) - 1));
     if (mf) *mf = (int64_t)(qp >> g->pack_shift);
+    return GR_OK;
+}
+
+gr_status gr_part_bfs_frontier_async(gr_graph *h, int32_t level, int64_t *out3) {
+    Graph *g = (Graph *)h;
+    if (!g || !g->part || level < 0 || !out3 || !ptr_on_device(out3)) {
+        set_error("invalid argument (out3 must be device int64[3])");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    part_frontier_kernel<<<1, 1, 0, g->stream>>>(g->ctl, level, g->pack_shift, (long long *)out3);
+    count_launch();
+    GR_CUDA(cudaGetLastError());
     return GR_OK;
 }
 

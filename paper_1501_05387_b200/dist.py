@@ -143,6 +143,15 @@ class GpuPartition:
         _check(load().gr_part_bfs_frontier(self.handle, level, ctypes.byref(f), ctypes.byref(mf)))
         return f.value, mf.value
 
+    def frontier_dev(self, level: int) -> torch.Tensor:
+        """{f, m_f, overflow} of level `level` as a DEVICE int64[3] tensor,
+        written on the partition's stream without a host synchronisation
+        (gr_part_bfs_frontier_async); the caller all-reduces it."""
+        if getattr(self, "_fbuf", None) is None:
+            self._fbuf = torch.zeros(3, dtype=torch.int64, device=torch.device("cuda", self.device))
+        _check(load().gr_part_bfs_frontier_async(self.handle, level, self._fbuf.data_ptr()))
+        return self._fbuf
+
     def degree(self, v_global: int) -> int:
         """Out-degree of an owned vertex (0 if not owned)."""
         if self.v_begin <= v_global < self.v_end:
@@ -252,6 +261,23 @@ def decide_direction(direction: str, cur: str, f: int, mf: int, u: int, m_u: int
     return "push" if (f < nonisolated / beta and f < prev_f) else "pull"
 
 
+def _global_frontier(part, exchange, level: int, dev):
+    """Global (f, m_f) of `level`: the local counters are summed over ranks on
+    the device and read with ONE host synchronisation (the partition's
+    frontier_dev when it has one; otherwise its host frontier())."""
+    fd = getattr(part, "frontier_dev", None)
+    if fd is not None:
+        loc = fd(level).clone()
+    else:
+        lf, lmf = part.frontier(level)
+        loc = torch.tensor([lf, lmf, 0], dtype=torch.int64, device=dev)
+    f, mf, ov = exchange.allreduce_sum(loc).tolist()
+    if ov:
+        raise GrError(5, "overflow on some rank (local frontier queue overflow or a received "
+                         "vertex the rank does not own)")  # 5 = GR_ERR_OVERFLOW
+    return f, mf
+
+
 def bfs_partitioned(part, exchange, src: int, depth: torch.Tensor, pred: torch.Tensor = None,
                     direction: str = "auto", max_levels: int = 1 << 30, trace: list = None):
     """Runs one BFS over the partition of this rank (all ranks call it with the
@@ -277,8 +303,8 @@ def bfs_partitioned(part, exchange, src: int, depth: torch.Tensor, pred: torch.T
             part.expand(level)
             sc = part.send_counts.clone() if part.send_counts.device == dev else part.send_counts.to(dev)
             rc = exchange.counts(sc)
-            sc_h = sc.tolist()
-            rc_h = rc.tolist()
+            both = torch.cat([sc, rc]).tolist()  # one host read for both count vectors
+            sc_h, rc_h = both[: len(both) // 2], both[len(both) // 2:]
             send_flat = _gather_buckets(part, sc_h)
             nrecv = int(sum(rc_h))
             out = part.recv_pairs[: 2 * nrecv]
@@ -290,9 +316,7 @@ def bfs_partitioned(part, exchange, src: int, depth: torch.Tensor, pred: torch.T
             part.pull(level, part.global_buf)
         level += 1
         prev_f = f
-        lf, lmf = part.frontier(level)
-        tot = exchange.allreduce_sum(torch.tensor([lf, lmf], dtype=torch.int64, device=dev)).tolist()
-        f, mf = tot
+        f, mf = _global_frontier(part, exchange, level, dev)
         u -= f  # symmetric graphs: every discovered vertex has out-degree > 0
         m_u -= mf
     return level
@@ -326,7 +350,8 @@ def sssp_partitioned(part, exchange, src: int, dist: torch.Tensor, pred: torch.T
             part.sssp_relax(k, it, fp, thr)
             sc = part.send_counts.clone() if part.send_counts.device == dev else part.send_counts.to(dev)
             rc = exchange.counts(sc)
-            sc_h, rc_h = sc.tolist(), rc.tolist()
+            both = torch.cat([sc, rc]).tolist()  # one host read for both count vectors
+            sc_h, rc_h = both[: len(both) // 2], both[len(both) // 2:]
             B = part.block
             send_flat = torch.cat([part.send_triples[3 * q * B: 3 * q * B + 3 * int(c)]
                                    for q, c in enumerate(sc_h)])
