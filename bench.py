@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--keep-order", action="store_true",
+                    help="partitioned BFS: keep the caller's pull-list order (no gr_part_order_pull_lists)")
     ap.add_argument("--partitioned", action="store_true",
                     help="1D-partitioned BFS / SSSP over all ranks (NCCL exchange per step); "
                          "default graph c5_kron25 (BFS) / c3_orkut (SSSP)")
@@ -265,6 +267,8 @@ def run_partitioned(args, rank, world, dev):
     del g
     torch.cuda.empty_cache()
     ex = grd.TorchDistExchange()
+    if not sssp and not args.keep_order:  # pull lists by global neighbour degree (a7; as on one GPU)
+        part.order_pull_lists(grd.global_degrees(part, ex))
     depth = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
     pred = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -312,6 +316,8 @@ def run_partitioned(args, rank, world, dev):
                                        "of the frontier bitmap" % args.config),
                           "graph": CONFIG_DESC[args.config], "n": n, "m": m,
                           "parallelism": "1D vertex partition over %d rank(s)" % world,
+                          "pull_lists": "caller order" if (sssp or args.keep_order)
+                          else "ordered by global neighbour degree (gr_part_order_pull_lists)",
                           "l2": "flushed (256 MiB write) between timed steps"},
                "gpu_launches": launches, "levels_per_step": sum(levels) / len(levels),
                "clocks": clk.summary(),

@@ -336,9 +336,23 @@ gr_status gr_part_bfs_frontier_async(gr_graph *g, int32_t level, int64_t *out3);
  *   gr_part_bfs_pull   bottom-up step over the owned unvisited vertices
  *                      against that global bitmap; builds the local frontier
  *                      of level+1 (no exchange needed: parents are global ids).
- * block is a multiple of 32 (block = 32*ceil(n/(32*nparts))). */
+ * block is a multiple of 32 (block = 32*ceil(n/(32*nparts))). When the
+ * frontier of `level` was built by gr_part_bfs_pull(level-1), the pull step
+ * already wrote its shard (one ballot word per warp) and gr_part_bfs_shard is
+ * a device copy of it; otherwise the shard is built from the local queue. */
 gr_status gr_part_bfs_shard(gr_graph *g, int32_t level, uint32_t *shard);
 gr_status gr_part_bfs_pull(gr_graph *g, int32_t level, const uint32_t *global_frontier);
+/* Optional, once after gr_graph_create_part on a symmetric partition: orders
+ * each owned vertex's pull list by the GLOBAL out-degree of the neighbour,
+ * descending (a sorted copy; push lists keep the caller's order), so the
+ * early exit of gr_part_bfs_pull finds a frontier parent sooner (the single-GPU
+ * create does the same). Results are unchanged:
+ * any order of a list is the same graph. deg_global: DEVICE int32[n_global],
+ * out-degree of every global vertex (the all-gather of every rank's local
+ * degrees), read during the call only. Returns GR_ERR_INVALID_ARGUMENT for a
+ * host pointer, a non-symmetric partition or m_local >= 2^31; synchronises the
+ * graph's stream. */
+gr_status gr_part_order_pull_lists(gr_graph *g, const int32_t *deg_global);
 
 /* ===========================================================================
  * Multi-GPU SSSP over the same 1D partition. The paper's
@@ -393,6 +407,12 @@ gr_status gr_part_sssp_absorb(gr_graph *g, int32_t step, int32_t it, int32_t fp,
                               const int32_t *recv_triples, int64_t nrecv);
 gr_status gr_part_sssp_counts(gr_graph *g, int32_t step, int32_t fp, int64_t *near_count,
                               int64_t *far_count);
+/* As gr_part_sssp_counts without a host synchronisation: enqueues a write of
+ * {near count of step, far count of pile fp, overflow code} to DEVICE int64
+ * out3[3] on the graph's stream; the caller sums it over ranks (one NCCL
+ * all-reduce) and treats overflow != 0 as GR_ERR_OVERFLOW. Host out3 is
+ * rejected with GR_ERR_INVALID_ARGUMENT. */
+gr_status gr_part_sssp_counts_async(gr_graph *g, int32_t step, int32_t fp, int64_t *out3);
 gr_status gr_part_sssp_far_min(gr_graph *g, int32_t step, int32_t fp, uint64_t thr, uint64_t *min_out);
 gr_status gr_part_sssp_resplit(gr_graph *g, int32_t step, int32_t it, int32_t fp, uint64_t thr_old,
                                uint64_t thr);

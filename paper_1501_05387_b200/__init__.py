@@ -71,9 +71,9 @@ EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_gra
            "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
            "gr_get_run_stats", "gr_last_error", "gr_kernel_launch_count",
            "gr_version", "gr_graph_create_part", "gr_part_buffers", "gr_part_bfs_begin",
-           "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_bfs_shard",
+           "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_order_pull_lists", "gr_part_bfs_shard",
            "gr_part_bfs_pull", "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
-           "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_far_min",
+           "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_counts_async", "gr_part_sssp_counts_async", "gr_part_sssp_far_min",
            "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank"]
 
 
@@ -113,6 +113,7 @@ def load(path: str = LIB_PATH):
     lib.gr_part_bfs_absorb.argtypes = [p, i32, p, i64]
     lib.gr_part_bfs_frontier.argtypes = [p, i32, P(i64), P(i64)]
     lib.gr_part_bfs_frontier_async.argtypes = [p, i32, p]
+    lib.gr_part_order_pull_lists.argtypes = [p, p]
     lib.gr_part_bfs_shard.argtypes = [p, i32, p]
     lib.gr_part_bfs_pull.argtypes = [p, i32, p]
     u64 = ctypes.c_uint64
@@ -123,6 +124,7 @@ def load(path: str = LIB_PATH):
     lib.gr_part_sssp_relax.argtypes = [p, i32, i32, i32, u64]
     lib.gr_part_sssp_absorb.argtypes = [p, i32, i32, i32, u64, p, i64]
     lib.gr_part_sssp_counts.argtypes = [p, i32, i32, P(i64), P(i64)]
+    lib.gr_part_sssp_counts_async.argtypes = [p, i32, i32, p]
     lib.gr_part_sssp_far_min.argtypes = [p, i32, i32, u64, P(u64)]
     lib.gr_part_sssp_resplit.argtypes = [p, i32, i32, i32, u64, u64]
     lib.gr_part_sssp_end.argtypes = [p]
@@ -133,7 +135,7 @@ def load(path: str = LIB_PATH):
               "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
               "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
               "gr_part_bfs_begin", "gr_part_bfs_expand", "gr_part_bfs_absorb",
-              "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_bfs_shard", "gr_part_bfs_pull",
+              "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_order_pull_lists", "gr_part_bfs_shard", "gr_part_bfs_pull",
               "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
               "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts",
               "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank"):

@@ -131,6 +131,8 @@ struct Graph {
     long long *send_counts = nullptr;  // [nparts]
     int32_t *recv_pairs = nullptr;     // [2 * n_global]
     int32_t *part_depth = nullptr, *part_pred = nullptr;
+    uint32_t *pull_shard = nullptr;   // [block/32] frontier shard written by the last pull step
+    int32_t pull_shard_level = -1;     // the level whose frontier pull_shard holds (-1: none)
     // partitioned SSSP (partition_sssp.cu)
     unsigned long long *ps_best = nullptr;  // [n_global] best (dist<<32|pred) shipped per remote vertex
     int32_t *ps_sstamp = nullptr;           // [n_global] step of the last shipment (one per step)

@@ -15,6 +15,7 @@ namespace gr {
 gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C, const uint32_t *W,
                        uint32_t flags, int device, void *stream, Graph **out, int64_t ncols);
 bool ptr_on_device(const void *p);
+gr_status sort_lists_by_degree(Graph *g, cudaStream_t s, int blocks, const int32_t *deg);
 
 constexpr int kPartBlock = 256;
 constexpr int kPartWarps = kPartBlock / 32;
@@ -26,6 +27,7 @@ struct PartArgs {
     int nparts;
     const int64_t *R;
     const int32_t *C;
+    const int32_t *Cp;   // pull lists: C, or its copy ordered by neighbour degree
     uint32_t *visited;   // local bitmap
     uint32_t *sent;      // global bitmap
     int32_t *send_pairs;
@@ -214,7 +216,8 @@ __global__ void part_shard_fill_kernel(PartArgs a, int level, uint32_t *shard) {
 // a parent in the GLOBAL frontier bitmap; a warp owns one 32-vertex word of the
 // local visited bitmap (ballot + store, no atomics); discovered vertices join
 // the local queue of level + 1 (merge-path prefix via the packed counter).
-__global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int level, const uint32_t *gfront) {
+__global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int level, const uint32_t *gfront,
+                                                              uint32_t *nshard) {
     __shared__ int32_t s_v[kPartWarps][kPartStage];
     __shared__ int32_t s_d[kPartWarps][kPartStage];
     __shared__ int64_t s_r[kPartWarps][kPartStage];
@@ -247,7 +250,7 @@ __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int l
             int32_t u[4];
             uint32_t fw[4];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = (e + k < end) ? ld_stream(a.C + e + k, pol) : -1;
+            for (int k = 0; k < 4; ++k) u[k] = (e + k < end) ? ld_stream(a.Cp + e + k, pol) : -1;
 #pragma unroll
             for (int k = 0; k < 4; ++k) fw[k] = (u[k] >= 0) ? __ldg(gfront + (u[k] >> 5)) : 0u;
 #pragma unroll
@@ -256,6 +259,9 @@ __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int l
         }
         const unsigned nb = __ballot_sync(0xffffffffu, found);
         if (l == 0 && nb) a.visited[wi] = visw | nb;
+        // the level+1 frontier shard word (found vertices have in-edges, hence
+        // out-degree > 0 on a symmetric graph: exactly the queued set)
+        if (l == 0) nshard[wi] = nb;
         int64_t deg = 0;
         if (found) {
             a.depth[v] = level + 1;
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int l
 static PartArgs part_args(Graph *g) {
     PartArgs a;
     a.n_local = g->n; a.v_begin = g->v_begin; a.block = g->block; a.nparts = g->nparts;
-    a.R = g->R; a.C = g->C; a.visited = g->visited; a.sent = g->sent;
+    a.R = g->R; a.C = g->C; a.Cp = g->Ct; a.visited = g->visited; a.sent = g->sent;
     a.send_pairs = g->send_pairs; a.send_counts = g->send_counts;
     a.depth = g->part_depth; a.pred = g->part_pred;
     for (int i = 0; i < 2; ++i) { a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.qr[i] = g->qr[i]; }
@@ -373,6 +379,7 @@ gr_status gr_part_bfs_begin(gr_graph *h, int64_t src, int32_t *depth_out, int32_
     }
     g->part_depth = depth_out;
     g->part_pred = pred_out;
+    g->pull_shard_level = -1;
     PartArgs a = part_args(g);
     part_init_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(a, (g->n_global + 31) / 32);
     part_seed_kernel<<<1, 1, 0, g->stream>>>(a, src);
@@ -384,6 +391,7 @@ gr_status gr_part_bfs_begin(gr_graph *h, int64_t src, int32_t *depth_out, int32_
 gr_status gr_part_bfs_expand(gr_graph *h, int32_t level) {
     Graph *g = (Graph *)h;
     if (!g || !g->part || level < 0) { set_error("invalid argument"); return GR_ERR_INVALID_ARGUMENT; }
+    if (g->pull_shard_level == level + 1) g->pull_shard_level = -1;  // level+1 is rebuilt by push
     PartArgs a = part_args(g);
     GR_CUDA(cudaMemsetAsync(g->send_counts, 0, g->nparts * sizeof(long long), g->stream));
     part_expand_kernel<<<g->num_sms * 8, kPartBlock, 0, g->stream>>>(a, level);
@@ -411,6 +419,11 @@ gr_status gr_part_bfs_absorb(gr_graph *h, int32_t level, const int32_t *recv_pai
 gr_status gr_part_bfs_shard(gr_graph *h, int32_t level, uint32_t *shard) {
     Graph *g = (Graph *)h;
     if (!g || !g->part || level < 0 || !shard) { set_error("invalid argument"); return GR_ERR_INVALID_ARGUMENT; }
+    if (g->pull_shard_level == level) {  // written by the pull step that built this frontier
+        GR_CUDA(cudaMemcpyAsync(shard, g->pull_shard, (g->block / 32) * sizeof(uint32_t), cudaMemcpyDeviceToDevice,
+                                g->stream));
+        return GR_OK;
+    }
     PartArgs a = part_args(g);
     part_shard_clear_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(shard, g->block / 32);
     part_shard_fill_kernel<<<g->num_sms * 2, 256, 0, g->stream>>>(a, level, shard);
@@ -422,9 +435,15 @@ gr_status gr_part_bfs_shard(gr_graph *h, int32_t level, uint32_t *shard) {
 gr_status gr_part_bfs_pull(gr_graph *h, int32_t level, const uint32_t *global_frontier) {
     Graph *g = (Graph *)h;
     if (!g || !g->part || level < 0 || !global_frontier) { set_error("invalid argument"); return GR_ERR_INVALID_ARGUMENT; }
+    if (!g->pull_shard) {
+        gr_status st = dev_alloc(g, (void **)&g->pull_shard, (g->block / 32) * sizeof(uint32_t));
+        if (st != GR_OK) return st;
+        GR_CUDA(cudaMemsetAsync(g->pull_shard, 0, (g->block / 32) * sizeof(uint32_t), g->stream));
+    }
     PartArgs a = part_args(g);
-    part_pull_kernel<<<g->num_sms * 8, kPartBlock, 0, g->stream>>>(a, level, global_frontier);
+    part_pull_kernel<<<g->num_sms * 8, kPartBlock, 0, g->stream>>>(a, level, global_frontier, g->pull_shard);
     count_launch();
+    g->pull_shard_level = level + 1;
     GR_CUDA(cudaGetLastError());
     return GR_OK;
 }
@@ -455,6 +474,29 @@ gr_status gr_part_bfs_frontier_async(gr_graph *h, int32_t level, int64_t *out3) 
     count_launch();
     GR_CUDA(cudaGetLastError());
     return GR_OK;
+}
+
+gr_status gr_part_order_pull_lists(gr_graph *h, const int32_t *deg_global) {
+    Graph *g = (Graph *)h;
+    if (!g || !g->part || !deg_global || !ptr_on_device(deg_global)) {
+        set_error("invalid argument (deg_global must be device int32[n_global])");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    if (g->Rt != g->R) {
+        set_error("pull-list order needs a symmetric partition (out-lists double as in-lists)");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    if (g->m == 0) return GR_OK;
+    if (g->m >= (1ll << 31)) {
+        set_error("pull-list order: m_local >= 2^31 is not supported by the segmented sort");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    if (g->Ct == g->C) {
+        gr_status st = dev_alloc(g, (void **)&g->Ct, g->m * sizeof(int32_t));
+        if (st != GR_OK) { g->Ct = g->C; return st; }
+        GR_CUDA(cudaMemcpyAsync(g->Ct, g->C, g->m * sizeof(int32_t), cudaMemcpyDeviceToDevice, g->stream));
+    }
+    return sort_lists_by_degree(g, g->stream, g->num_sms * 4, deg_global);
 }
 
 }  // extern "C"

@@ -342,6 +342,14 @@ static gr_status ps_check(Graph *g, bool begun = true) {
 
 using namespace gr;
 
+// Device-side counters (no host synchronisation): out = {near count of step,
+// far count of pile fp, overflow code}; summed over ranks by the caller.
+__global__ void ps_counts_kernel(const gr::Ctl *ctl, int step, int fp, int S, long long *out) {
+    out[0] = (long long)(ctl->slot[step & 3].qpack & ((1ull << S) - 1));
+    out[1] = (long long)ctl->far_count[fp];
+    out[2] = (long long)ctl->overflow;
+}
+
 extern "C" {
 
 gr_status gr_part_sssp_begin(gr_graph *h, int64_t src, uint32_t *dist_out, int32_t *pred_out) {
@@ -485,6 +493,20 @@ gr_status gr_part_sssp_end(gr_graph *h) {
     count_launch();
     GR_CUDA(cudaGetLastError());
     GR_CUDA(cudaStreamSynchronize(g->stream));
+    return GR_OK;
+}
+
+gr_status gr_part_sssp_counts_async(gr_graph *h, int32_t step, int32_t fp, int64_t *out3) {
+    Graph *g = (Graph *)h;
+    gr_status st = ps_check(g);
+    if (st != GR_OK) return st;
+    if (step < 0 || (fp & ~1) || !out3 || !ptr_on_device(out3)) {
+        set_error("invalid step/fp or out3 (device int64[3])");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    ps_counts_kernel<<<1, 1, 0, g->stream>>>(g->ctl, step, fp, g->pack_shift, (long long *)out3);
+    count_launch();
+    GR_CUDA(cudaGetLastError());
     return GR_OK;
 }
 

@@ -30,6 +30,7 @@ import torch
 
 from . import GrError, _check, _ptr, load
 
+GR_SYMMETRIC = 1
 GR_VALIDATE = 4
 NO_FAR = (1 << 63) - 1   # "no live far entry" (int64 max: all-reducible as int64)
 
@@ -88,13 +89,13 @@ class GpuPartition:
         if W_local is None:
             _check(load().gr_graph_create_part(n_global, nparts, rank, self.v_begin, self.v_end,
                                                int(C_local.numel()), rp, cp,
-                                               GR_VALIDATE if validate else 0, device,
+                                               (GR_VALIDATE if validate else 0) | (GR_SYMMETRIC if symmetric else 0), device,
                                                ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
         else:
             wp, wk = _ptr(W_local)
             _check(load().gr_graph_create_part_w(n_global, nparts, rank, self.v_begin, self.v_end,
                                                  int(C_local.numel()), rp, cp, wp,
-                                                 GR_VALIDATE if validate else 0, device,
+                                                 (GR_VALIDATE if validate else 0) | (GR_SYMMETRIC if symmetric else 0), device,
                                                  ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
         self.weighted = W_local is not None
         self._ps = None
@@ -142,6 +143,12 @@ class GpuPartition:
         f, mf = ctypes.c_int64(), ctypes.c_int64()
         _check(load().gr_part_bfs_frontier(self.handle, level, ctypes.byref(f), ctypes.byref(mf)))
         return f.value, mf.value
+
+    def order_pull_lists(self, deg_global: torch.Tensor):
+        """Pull lists ordered by global neighbour degree (gr_part_order_pull_lists);
+        deg_global: device int32[n_global]."""
+        assert deg_global.dtype == torch.int32 and deg_global.numel() == self.n_global and deg_global.is_cuda
+        _check(load().gr_part_order_pull_lists(self.handle, deg_global.data_ptr()))
 
     def frontier_dev(self, level: int) -> torch.Tensor:
         """{f, m_f, overflow} of level `level` as a DEVICE int64[3] tensor,
@@ -193,6 +200,14 @@ class GpuPartition:
         _check(load().gr_part_sssp_counts(self.handle, step, fp, ctypes.byref(f), ctypes.byref(fc)))
         return f.value, fc.value
 
+    def sssp_counts_dev(self, step: int, fp: int) -> torch.Tensor:
+        """{near, far, overflow} as a DEVICE int64[3] tensor, no host sync
+        (gr_part_sssp_counts_async); the caller all-reduces it."""
+        if getattr(self, "_cbuf", None) is None:
+            self._cbuf = torch.zeros(3, dtype=torch.int64, device=torch.device("cuda", self.device))
+        _check(load().gr_part_sssp_counts_async(self.handle, step, fp, self._cbuf.data_ptr()))
+        return self._cbuf
+
     def sssp_far_min(self, step: int, fp: int, thr: int) -> int:
         mn = ctypes.c_uint64()
         _check(load().gr_part_sssp_far_min(self.handle, step, fp, thr, ctypes.byref(mn)))
@@ -203,6 +218,18 @@ class GpuPartition:
 
     def sssp_end(self):
         _check(load().gr_part_sssp_end(self.handle))
+
+
+def global_degrees(part, exchange) -> torch.Tensor:
+    """int32[n_global] out-degree of every global vertex on this rank's device:
+    the all-gather of every rank's local degrees (blocks are padded to
+    `block`, the padding sliced off)."""
+    dev = torch.device("cuda", part.device) if isinstance(part.device, int) else part.device
+    loc = torch.zeros(part.block, dtype=torch.int32, device=dev)
+    loc[: part.n_local] = part._deg.to(device=dev, dtype=torch.int32)
+    out = torch.empty(part.nparts * part.block, dtype=torch.int32, device=dev)
+    exchange.allgather(loc, out)
+    return out[: part.n_global].contiguous()
 
 
 class TorchDistExchange:
@@ -328,6 +355,21 @@ def next_threshold(mn: int, delta: int) -> int:
     return (mn // delta + 1) * delta
 
 
+def _global_near(part, exchange, step: int, fp: int, dev) -> int:
+    """Global near-queue size of `step`: local counters summed over ranks on
+    the device, one host read (sssp_counts_dev when the partition has it)."""
+    cd = getattr(part, "sssp_counts_dev", None)
+    if cd is not None:
+        loc = cd(step, fp).clone()
+    else:
+        loc = torch.tensor([part.sssp_counts(step, fp)[0], 0, 0], dtype=torch.int64, device=dev)
+    near, _, ov = exchange.allreduce_sum(loc).tolist()
+    if ov:
+        raise GrError(5, "overflow on some rank (a near/far queue exceeded its capacity or a received "
+                         "vertex the rank does not own)")  # 5 = GR_ERR_OVERFLOW
+    return near
+
+
 def sssp_partitioned(part, exchange, src: int, dist: torch.Tensor, pred: torch.Tensor = None,
                      delta: int = 1, trace: list = None):
     """Near/far delta-stepping SSSP (Alg. 1) over the 1D
@@ -340,8 +382,7 @@ def sssp_partitioned(part, exchange, src: int, dist: torch.Tensor, pred: torch.T
     dev = dist.device
     part.sssp_begin(src, dist, pred)
     k, it, fp, thr = 0, 0, 0, int(delta)
-    f = int(exchange.allreduce_sum(torch.tensor([part.sssp_counts(0, fp)[0]], dtype=torch.int64,
-                                                device=dev)).item())
+    f = _global_near(part, exchange, 0, fp, dev)
     while True:
         if f > 0:
             it += 1
@@ -371,8 +412,7 @@ def sssp_partitioned(part, exchange, src: int, dist: torch.Tensor, pred: torch.T
             part.sssp_resplit(k, it, fp, thr_old, thr)
             fp ^= 1
         k += 1
-        f = int(exchange.allreduce_sum(torch.tensor([part.sssp_counts(k, fp)[0]], dtype=torch.int64,
-                                                    device=dev)).item())
+        f = _global_near(part, exchange, k, fp, dev)
     part.sssp_end()
     return k
 

@@ -30,11 +30,14 @@ def grd():
     return dist
 
 
-def _loopback(grd, g, P, srcs, directions=("push", "pull", "auto")):
+def _loopback(grd, g, P, srcs, directions=("push", "pull", "auto"), ordered=False):
     parts = []
+    deg_global = (g.R[1:] - g.R[:-1]).to(torch.int32).cuda()
     for r in range(P):
         v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, P, r)
         parts.append(grd.GpuPartition(Rl.cuda(), Cl.cuda(), g.n, P, r, symmetric=g.symmetric))
+        if ordered:
+            parts[-1].order_pull_lists(deg_global)
     grp = grd.LoopbackGroup(parts)
     R, C, _ = g.numpy()
     if not g.symmetric:
@@ -72,6 +75,25 @@ def test_loopback_kron_scale18(grd):
     _loopback(grd, g, 4, gg.sources(g, 2))
 
 
+@pytest.mark.parametrize("P", [1, 3, 4])
+def test_loopback_ordered_pull_lists(grd, P):
+    """gr_part_order_pull_lists: pull lists sorted by global neighbour degree
+    (a copy; push lists untouched) -- depths stay bit-exact, preds valid."""
+    g = gg.kronecker(16, 16, seed=2)
+    _loopback(grd, g, P, [0] + gg.sources(g, 2), ordered=True)
+
+
+def test_order_pull_lists_errors(grd):
+    import paper_1501_05387_b200 as gr
+    g = gg.directed_random(2000, 10000, seed=4)
+    v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, 2, 0)
+    pt = grd.GpuPartition(Rl.cuda(), Cl.cuda(), g.n, 2, 0, symmetric=False)
+    deg = (g.R[1:] - g.R[:-1]).to(torch.int32)
+    with pytest.raises(gr.GrError):  # host degree array
+        gr._check(gr.load().gr_part_order_pull_lists(pt.handle, deg.data_ptr()))
+    pt.close()
+
+
 def _port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -90,6 +112,9 @@ def test_world1_nccl_group(grd):
         v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, 1, 0)
         part = grd.GpuPartition(Rl.cuda(), Cl.cuda(), g.n, 1, 0)
         ex = grd.TorchDistExchange()
+        dg = grd.global_degrees(part, ex)
+        assert torch.equal(dg.cpu(), (g.R[1:] - g.R[:-1]).to(torch.int32))
+        part.order_pull_lists(dg)
         R, C, _ = g.numpy()
         for s, direction in [(s, d) for s in gg.sources(g, 2) for d in ("push", "pull", "auto")]:
             depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
