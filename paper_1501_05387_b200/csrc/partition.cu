@@ -213,14 +213,25 @@ __global__ void part_shard_fill_kernel(PartArgs a, int level, uint32_t *shard) {
 }
 
 // Bottom-up step of a partition: owned unvisited vertices look for
-// a parent in the GLOBAL frontier bitmap; a warp owns one 32-vertex word of the
-// local visited bitmap (ballot + store, no atomics); discovered vertices join
-// the local queue of level + 1 (merge-path prefix via the packed counter).
+// a parent in the GLOBAL frontier bitmap. As the single-GPU pull_level: each
+// warp compacts the unvisited vertices of 32 words of the local visited bitmap
+// into a shared-memory candidate list (ascending ids), then resolves 64
+// candidates at a time (2 per lane, the row-offset and first-neighbour loads
+// of both issued together); a lane scans up to kPartPullLong more edges of an
+// unresolved list, and whatever is left of the long lists is scanned by the
+// whole warp, 32 edges a step with a ballot early exit. Found vertices: depth /
+// pred, RED.OR into the local visited bitmap and into `nshard` (the level+1
+// frontier shard, cleared before the launch), and the local queue of level + 1
+// (merge-path prefix via the packed counter).
+constexpr int64_t kPartPullLong = 4;
+constexpr int kPartPullBatch = 64;
+
 __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int level, const uint32_t *gfront,
                                                               uint32_t *nshard) {
     __shared__ int32_t s_v[kPartWarps][kPartStage];
     __shared__ int32_t s_d[kPartWarps][kPartStage];
     __shared__ int64_t s_r[kPartWarps][kPartStage];
+    __shared__ int32_t s_wl[kPartWarps][kPartPullBatch + 32];
     const int wib = threadIdx.x >> 5;
     const unsigned l = lane_id();
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -237,39 +248,103 @@ __global__ void __launch_bounds__(kPartBlock) part_pull_kernel(PartArgs a, int l
     app.qo = a.qo[(level + 1) & 1];
     app.qr = a.qr[(level + 1) & 1];
     app.counter = &a.ctl->slot[(level + 1) & 3].qpack;
+    int32_t *wl = s_wl[wib];
     const unsigned long long pol = policy_evict_first();
     const int64_t nwords = (a.n_local + 31) / 32;
-    for (int64_t wi = gw; wi < nwords; wi += nw) {
-        const int64_t v = wi * 32 + l;
-        const uint32_t visw = a.visited[wi];
-        bool found = false;
-        int32_t parent = -1;
-        int64_t beg = 0, end = 0;
-        if (v < a.n_local && !((visw >> l) & 1u)) { beg = a.R[v]; end = a.R[v + 1]; }
-        for (int64_t e = beg; e < end && !found; e += 4) {
-            int32_t u[4];
-            uint32_t fw[4];
+    const uint32_t tail = (a.n_local & 31) ? ((1u << (a.n_local & 31)) - 1u) : 0xffffffffu;
+    auto fbit = [&](int32_t u) -> bool { return (__ldg(gfront + (u >> 5)) >> (u & 31)) & 1u; };
+    int cnt = 0;  // warp-uniform
+    auto process = [&](int k) {  // candidates wl[0, k), k <= kPartPullBatch
+        int32_t v[2], par[2], u0[2];
+        int64_t beg[2], end[2], nxt[2];
+        bool fnd[2];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) u[k] = (e + k < end) ? ld_stream(a.Cp + e + k, pol) : -1;
+        for (int q = 0; q < 2; ++q) v[q] = ((int)l + 32 * q < k) ? wl[l + 32 * q] : -1;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) fw[k] = (u[k] >= 0) ? __ldg(gfront + (u[k] >> 5)) : 0u;
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (!found && u[k] >= 0 && ((fw[k] >> (u[k] & 31)) & 1u)) { found = true; parent = u[k]; }
+        for (int q = 0; q < 2; ++q) {
+            beg[q] = v[q] >= 0 ? a.R[v[q]] : 0;
+            end[q] = v[q] >= 0 ? a.R[v[q] + 1] : 0;
         }
-        const unsigned nb = __ballot_sync(0xffffffffu, found);
-        if (l == 0 && nb) a.visited[wi] = visw | nb;
-        // the level+1 frontier shard word (found vertices have in-edges, hence
-        // out-degree > 0 on a symmetric graph: exactly the queued set)
-        if (l == 0) nshard[wi] = nb;
-        int64_t deg = 0;
-        if (found) {
-            a.depth[v] = level + 1;
-            if (a.pred) a.pred[v] = parent;
-            deg = end - beg;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Cp + beg[q], pol) : -1;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            fnd[q] = u0[q] >= 0 && fbit(u0[q]);
+            par[q] = u0[q];
         }
-        app.push(found && deg > 0, (int32_t)v, deg, beg);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            nxt[q] = beg[q] + 1;
+            if (fnd[q]) continue;
+            const int64_t lim = (end[q] - nxt[q] > kPartPullLong) ? nxt[q] + kPartPullLong : end[q];
+            for (int64_t e = nxt[q]; e < lim && !fnd[q]; e += 4) {
+                int32_t u[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) u[j] = (e + j < lim) ? ld_stream(a.Cp + e + j, pol) : -1;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (!fnd[q] && u[j] >= 0 && fbit(u[j])) { fnd[q] = true; par[q] = u[j]; }
+            }
+            nxt[q] = lim;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            unsigned lm = __ballot_sync(0xffffffffu, !fnd[q] && nxt[q] < end[q]);
+            while (lm) {
+                const int ld = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const int64_t b = __shfl_sync(0xffffffffu, nxt[q], ld);
+                const int64_t e = __shfl_sync(0xffffffffu, end[q], ld);
+                int32_t hitu = -1;
+                for (int64_t x = b; x < e; x += 32) {
+                    const int32_t u = (x + l < e) ? ld_stream(a.Cp + x + l, pol) : -1;
+                    const unsigned bm = __ballot_sync(0xffffffffu, u >= 0 && fbit(u));
+                    if (bm) {
+                        hitu = __shfl_sync(0xffffffffu, u, __ffs(bm) - 1);
+                        break;
+                    }
+                }
+                if ((int)l == ld && hitu >= 0) { fnd[q] = true; par[q] = hitu; }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            if (fnd[q]) {
+                const int32_t x = v[q];
+                a.depth[x] = level + 1;
+                if (a.pred) a.pred[x] = par[q];
+                const uint32_t bit = 1u << (x & 31);
+                atomicOr(nshard + (x >> 5), bit);     // RED.OR
+                atomicOr(a.visited + (x >> 5), bit);  // RED.OR
+            }
+            // found vertices have an in-edge, hence out-degree > 0 (symmetric)
+            app.push(fnd[q], fnd[q] ? v[q] : 0, end[q] - beg[q], beg[q]);
+        }
+        // keep the unprocessed tail (cnt - k < 32 entries) at the front
+        __syncwarp();
+        const int rem = cnt - k;
+        const int32_t t = ((int)l < rem) ? wl[k + l] : 0;
+        __syncwarp();
+        if ((int)l < rem) wl[l] = t;
+        __syncwarp();
+        cnt = rem;
+    };
+    for (int64_t w0 = gw * 32; w0 < nwords; w0 += nw * 32) {
+        const int64_t wi = w0 + l;
+        uint32_t cm = wi < nwords ? ~a.visited[wi] : 0u;
+        if (wi == nwords - 1) cm &= tail;
+        unsigned nz = __ballot_sync(0xffffffffu, cm != 0);
+        while (nz) {
+            const int j = __ffs(nz) - 1;
+            nz &= nz - 1;
+            const uint32_t w = __shfl_sync(0xffffffffu, cm, j);
+            if ((w >> l) & 1u) wl[cnt + __popc(w & lanemask_lt())] = (int32_t)((w0 + j) * 32 + l);
+            cnt += __popc(w);
+            __syncwarp();
+            if (cnt >= kPartPullBatch) process(kPartPullBatch);
+        }
     }
+    while (cnt > 0) process(cnt < kPartPullBatch ? cnt : kPartPullBatch);
     app.finish();
 }
 
@@ -440,6 +515,7 @@ gr_status gr_part_bfs_pull(gr_graph *h, int32_t level, const uint32_t *global_fr
         if (st != GR_OK) return st;
         GR_CUDA(cudaMemsetAsync(g->pull_shard, 0, (g->block / 32) * sizeof(uint32_t), g->stream));
     }
+    GR_CUDA(cudaMemsetAsync(g->pull_shard, 0, (g->block / 32) * sizeof(uint32_t), g->stream));
     PartArgs a = part_args(g);
     part_pull_kernel<<<g->num_sms * 8, kPartBlock, 0, g->stream>>>(a, level, global_frontier, g->pull_shard);
     count_launch();
