@@ -91,15 +91,19 @@ __device__ __forceinline__ void ps_reset_slot(const PsArgs &a, int step) {
 // Owner-side relaxation of local vertex lv with candidate (nd, parent):
 // UpdateLabel + SetPred (packed atomicMin, A-9) + RemoveRedundant (A-7) +
 // near/far split. Returns 1 near, 2 far, 0 nothing to append.
-__device__ __forceinline__ int ps_relax_owned(const PsArgs &a, int64_t lv, unsigned long long nd, uint32_t parent,
-                                              uint64_t thr, int32_t key_near, unsigned long long pol) {
-    if (nd >= (ld_probe(a.dp + lv, pol) >> 32)) return 0;  // plain pre-check
+__device__ __forceinline__ int ps_relax_owned_cur(const PsArgs &a, int64_t lv, unsigned long long nd, uint32_t parent,
+                                                  uint64_t thr, int32_t key_near, unsigned long long cur) {
+    if (nd >= (cur >> 32)) return 0;  // plain pre-check against the value loaded by the caller
     const unsigned long long old = atomicMin(a.dp + lv, (nd << 32) | parent);
     if (nd >= (old >> 32)) return 0;
     const bool far = nd >= thr;
     const int32_t key = key_near + (far ? 1 : 0);
     if (atomicExch(a.stamp + lv, key) == key) return 0;
     return far ? 2 : 1;
+}
+__device__ __forceinline__ int ps_relax_owned(const PsArgs &a, int64_t lv, unsigned long long nd, uint32_t parent,
+                                              uint64_t thr, int32_t key_near, unsigned long long pol) {
+    return ps_relax_owned_cur(a, lv, nd, parent, thr, key_near, ld_probe(a.dp + lv, pol));
 }
 
 struct PsRelaxOp {
@@ -116,8 +120,17 @@ struct PsRelaxOp {
     __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *du,
                                           const int32_t *dst, const T5 *x) {
         uint32_t w[U];
+        unsigned long long cur[U];
+        // all weight loads and all pre-check probes (dist of owned targets,
+        // best-shipped of remote ones) issued before any dependent atomic, as
+        // in the single-GPU RelaxOp
 #pragma unroll
-        for (int u = 0; u < U; ++u) w[u] = ok[u] ? __ldg(a->W + x[u]) : 0u;
+        for (int u = 0; u < U; ++u) {
+            w[u] = ok[u] ? __ldg(a->W + x[u]) : 0u;
+            const int64_t lv = (int64_t)dst[u] - a->v_begin;
+            const bool owned = lv >= 0 && lv < a->n_local;
+            cur[u] = ok[u] ? ld_probe(owned ? a->dp + lv : a->best + dst[u], pol) : 0ull;
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t v = dst[u];
@@ -129,9 +142,9 @@ struct PsRelaxOp {
             bool ship = false;
             int64_t deg = 0, rs = 0;
             if (ok[u] && owned) {
-                kind = ps_relax_owned(*a, lv, nd, parent, thr, key_near, pol);
+                kind = ps_relax_owned_cur(*a, lv, nd, parent, thr, key_near, cur[u]);
                 if (kind == 1) { rs = a->R[lv]; deg = a->R[lv + 1] - rs; }
-            } else if (ok[u] && nd < (ld_probe(a->best + v, pol) >> 32)) {
+            } else if (ok[u] && nd < (cur[u] >> 32)) {
                 const unsigned long long old = atomicMin(a->best + v, (nd << 32) | parent);
                 if (nd < (old >> 32)) ship = atomicExch(a->sstamp + v, step) != step;
             }
