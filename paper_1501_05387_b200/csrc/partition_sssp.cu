@@ -202,7 +202,7 @@ __global__ void ps_seed_kernel(PsArgs a, int64_t src) {
     }
 }
 
-__global__ void __launch_bounds__(kPsBlock) ps_relax_kernel(PsArgs a, int step, int it, int fp, uint64_t thr) {
+__global__ void __launch_bounds__(kPsBlock, 4) ps_relax_kernel(PsArgs a, int step, int it, int fp, uint64_t thr) {
     __shared__ PsSmem s;
     const int wib = threadIdx.x >> 5;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
