@@ -203,9 +203,13 @@ typedef struct {
     int32_t num_levels;            /* levels executed (may exceed records kept)    */
     int32_t num_records;           /* records available in levels[]                */
     const gr_level_stats *levels;  /* valid until the next run / destroy           */
-    int64_t reached;               /* vertices reached                             */
+    int64_t reached;               /* vertices reached (depth >= 0 / dist < inf),
+                                      counted on the device at the first query    */
     uint32_t delta;                /* SSSP: delta used                             */
     int32_t kernel_launches;       /* kernels launched by the last run            */
+    int64_t reached_edges;         /* directed edges whose source is reached: the
+                                      TEPS numerator m_reached (reading A-14; the
+                                      paper's Table 3 MTEPS = |E| / t) */
 } gr_run_stats;
 
 gr_status gr_get_run_stats(gr_graph *g, gr_run_stats *out);
@@ -264,6 +268,79 @@ gr_status gr_cc(gr_graph *g, int32_t *comp_out, int64_t *num_components);
  * =========================================================================== */
 gr_status gr_pagerank(gr_graph *g, double damping, double tol, int32_t max_iter, double *rank_out,
                       int32_t *iterations);
+
+/* ===========================================================================
+ * Multi-GPU group + partitioned graph. The paper is
+ * single-GPU and names multi-GPU as future work ("to multiple GPUs on a
+ * single node"); the method per partition is the single-GPU
+ * one above.
+ *
+ * gr_comm is one rank of a group of nranks <= 8 GPUs of one node, one process
+ * per GPU. The caller bootstraps the group: rank 0 calls
+ * gr_comm_get_unique_id, broadcasts the 128 bytes (e.g. torch.distributed),
+ * then every rank calls gr_comm_create with its rank and CUDA device. The
+ * library owns the ncclComm_t (NCCL of the calling process, libnccl.so.2) and
+ * uses it for the collective set-up steps; every traversal step, including
+ * the exchange between ranks, runs inside the library's kernels over peer
+ * memory (CUDA IPC mappings of each rank's symmetric region, NVLink).
+ *   gr_comm_get_unique_id  id_out: 128 writable bytes (ncclUniqueId).
+ *   gr_comm_create         collective over the nranks processes; errors:
+ *                          GR_ERR_INVALID_ARGUMENT (rank/nranks), GR_ERR_NCCL.
+ *   gr_comm_create_loopback  nranks VIRTUAL ranks in this process on one GPU
+ *                          (out: gr_comm*[nranks]). Collective calls on their
+ *                          graphs (gr_bfs) are joined: every rank's call is
+ *                          recorded and the call of the last rank runs all
+ *                          ranks in ONE launch, writes every rank's outputs and
+ *                          returns; the earlier calls return GR_OK at once with
+ *                          their outputs pending. For testing the multi-rank
+ *                          path on one GPU.
+ *   gr_comm_destroy        frees the handle (after the graphs using it).
+ *   gr_comm_info           rank, nranks, loopback flag (any output may be NULL).
+ * =========================================================================== */
+typedef struct gr_comm gr_comm;
+gr_status gr_comm_get_unique_id(void *id_out);
+gr_status gr_comm_create(int rank, int nranks, const void *nccl_unique_id, int device, gr_comm **out);
+gr_status gr_comm_create_loopback(int nranks, int device, gr_comm **out);
+gr_status gr_comm_destroy(gr_comm *c);
+gr_status gr_comm_info(const gr_comm *c, int32_t *rank, int32_t *nranks, int32_t *loopback);
+
+/*
+ * gr_graph_create_partitioned -- this rank's part of a symmetric graph with
+ * n_global vertices under a 1D vertex partition: rank q owns the block
+ * [q*B, min(n_global, (q+1)*B)), B = 32*ceil(n_global/(32*nranks)) (a multiple
+ * of 32 so bitmap shards concatenate), and stores the out-lists of its
+ * vertices with GLOBAL column ids (which double as in-lists for pull steps,
+ * hence GR_SYMMETRIC is required: "converted all datasets to
+ * undirected graphs").
+ *   v_begin, v_end  the owned block (checked against the formula above)
+ *   m_local         edges of the owned rows
+ *   row_offsets     int64[v_end - v_begin + 1], local rows, R[0] = 0
+ *   col_indices     int32[m_local], GLOBAL ids in [0, n_global)
+ *   weights         uint32[m_local] or NULL (reserved for a partitioned SSSP)
+ *   flags           GR_SYMMETRIC (required) | GR_VALIDATE | GR_KEEP_ORDER
+ *   cuda_stream     stream of this rank's work; the device is the comm's
+ * Copies its inputs. Collective for real ranks (the symmetric regions are
+ * mapped between the ranks here). Errors as gr_graph_create, plus
+ * GR_ERR_INVALID_ARGUMENT for a wrong block, a non-symmetric flag or a second
+ * graph on one loopback rank, GR_ERR_NCCL.
+ *
+ * gr_bfs(g, src, depth_out, pred_out, opts) on such a graph is COLLECTIVE
+ * (every rank calls it with the same GLOBAL src and opts): one persistent
+ * kernel per rank runs every level -- push levels ship remote discoveries
+ * straight into the owner's inbox, pull levels all-gather the frontier-bitmap
+ * shards with peer stores, and the per-level counters are exchanged the same
+ * way, so every rank takes the same direction decision (A-3) and stops at the
+ * same level; no host round trip per level. depth_out / pred_out: int32
+ * [v_end - v_begin] (host or device) for the OWNED block; pred holds GLOBAL
+ * ids. opts.strategy and opts.idempotent are ignored (merge-path advance,
+ * exactly-once claims). gr_get_run_stats: global per-level counters; `aux` of
+ * a level = bytes the level sent between ranks (push: 8 per shipped pair;
+ * pull: the shards); reached / reached_edges count the owned block.
+ * gr_bfs_async is not available for partitioned graphs.
+ */
+gr_status gr_graph_create_partitioned(gr_comm *c, int64_t n_global, int64_t v_begin, int64_t v_end,
+                                      int64_t m_local, const int64_t *row_offsets, const int32_t *col_indices,
+                                      const uint32_t *weights, uint32_t flags, void *cuda_stream, gr_graph **out);
 
 /* ===========================================================================
  * Multi-GPU: 1D vertex partition (the paper is single-GPU and

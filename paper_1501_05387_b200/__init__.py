@@ -63,7 +63,8 @@ class gr_level_stats(ctypes.Structure):
 class gr_run_stats(ctypes.Structure):
     _fields_ = [("num_levels", ctypes.c_int32), ("num_records", ctypes.c_int32),
                 ("levels", ctypes.POINTER(gr_level_stats)), ("reached", ctypes.c_int64),
-                ("delta", ctypes.c_uint32), ("kernel_launches", ctypes.c_int32)]
+                ("delta", ctypes.c_uint32), ("kernel_launches", ctypes.c_int32),
+                ("reached_edges", ctypes.c_int64)]
 
 
 _lib = None
@@ -73,8 +74,10 @@ EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_gra
            "gr_version", "gr_graph_create_part", "gr_part_buffers", "gr_part_bfs_begin",
            "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_order_pull_lists", "gr_part_bfs_shard",
            "gr_part_bfs_pull", "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
-           "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_counts_async", "gr_part_sssp_counts_async", "gr_part_sssp_far_min",
-           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank"]
+           "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_counts_async", "gr_part_sssp_far_min",
+           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank",
+           "gr_comm_get_unique_id", "gr_comm_create", "gr_comm_create_loopback", "gr_comm_destroy",
+           "gr_comm_info", "gr_graph_create_partitioned"]
 
 
 def load(path: str = LIB_PATH):
@@ -131,6 +134,12 @@ def load(path: str = LIB_PATH):
     lib.gr_bc.argtypes = [p, p, i64, p, p]
     lib.gr_cc.argtypes = [p, p, P(i64)]
     lib.gr_pagerank.argtypes = [p, ctypes.c_double, ctypes.c_double, i32, p, P(i32)]
+    lib.gr_comm_get_unique_id.argtypes = [p]
+    lib.gr_comm_create.argtypes = [ctypes.c_int, ctypes.c_int, p, ctypes.c_int, P(p)]
+    lib.gr_comm_create_loopback.argtypes = [ctypes.c_int, ctypes.c_int, p]
+    lib.gr_comm_destroy.argtypes = [p]
+    lib.gr_comm_info.argtypes = [p, P(i32), P(i32), P(i32)]
+    lib.gr_graph_create_partitioned.argtypes = [p, i64, i64, i64, i64, p, p, p, ctypes.c_uint32, p, P(p)]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
               "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
               "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
@@ -138,7 +147,9 @@ def load(path: str = LIB_PATH):
               "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_order_pull_lists", "gr_part_bfs_shard", "gr_part_bfs_pull",
               "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
               "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts",
-              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank"):
+              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank",
+              "gr_comm_get_unique_id", "gr_comm_create", "gr_comm_create_loopback", "gr_comm_destroy",
+              "gr_comm_info", "gr_graph_create_partitioned"):
         getattr(lib, f).restype = ctypes.c_int
     _lib = lib
     return lib
@@ -340,6 +351,7 @@ class Graph:
         st = gr_get_run_stats(self.handle)
         recs = [st.levels[i] for i in range(st.num_records)]
         return dict(num_levels=st.num_levels, delta=st.delta, kernel_launches=st.kernel_launches,
+                    reached=st.reached, reached_edges=st.reached_edges,
                     levels=[dict(level=r.level, direction=r.direction, frontier=r.frontier,
                                  frontier_edges=r.frontier_edges, discovered=r.discovered,
                                  inspected_edges=r.inspected_edges, aux=r.aux, ns=r.ns)

@@ -6,12 +6,28 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgr_b200.so")
-SOURCES = ["abi.cu", "graph.cu", "bfs.cu", "sssp.cu", "partition.cu", "partition_sssp.cu", "bc.cu", "cc.cu", "pagerank.cu"]
-HEADERS = ["gr_internal.cuh", "frontier.cuh", os.path.join("..", "..", "include", "gr.h")]
+SOURCES = ["abi.cu", "graph.cu", "bfs.cu", "sssp.cu", "partition.cu", "partition_sssp.cu", "bc.cu", "cc.cu", "pagerank.cu", "comm.cu", "pbfs.cu"]
+HEADERS = ["gr_internal.cuh", "frontier.cuh", "pull.cuh", os.path.join("..", "..", "include", "gr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+# NCCL: the library's own communicator (gr_comm_create) links the libnccl.so.2
+# torch ships (nvidia-nccl wheel), found again at run time through the rpath
+def _nccl_dir():
+    d = os.environ.get("GR_NCCL_DIR", "")
+    if d:
+        return d
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl")
+    for loc in (spec.submodule_search_locations or []) if spec else []:
+        if os.path.exists(os.path.join(loc, "include", "nccl.h")):
+            return loc
+    raise RuntimeError("nccl.h not found (set GR_NCCL_DIR to the nvidia/nccl directory)")
+
+
+NCCL_DIR = _nccl_dir()
 EXTRA = os.environ.get("GR_NVCC_EXTRA", "").split()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC", "-Xptxas", "-v", "-I" + os.path.join(NCCL_DIR, "include")]
+LDFLAGS = ["-Xlinker", os.path.join(NCCL_DIR, "lib", "libnccl.so.2"), "-Xlinker", "-rpath=" + os.path.join(NCCL_DIR, "lib")]
 
 
 def _stale(target, deps):
@@ -41,7 +57,7 @@ def build(force=False, verbose=False, lib=None):
             raise RuntimeError("nvcc failed on %s" % s)
         objs.append(o)
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs + LDFLAGS
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

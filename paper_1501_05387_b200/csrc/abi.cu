@@ -93,6 +93,10 @@ gr_status gr_graph_destroy(gr_graph *h) {
     Graph *g = (Graph *)h;
     cudaSetDevice(g->device);
     cudaStreamSynchronize(g->stream);
+    if (g->comm) {
+        if (g->comm->group && g->comm->group->graphs[g->comm->rank] == g) g->comm->group->graphs[g->comm->rank] = nullptr;
+        comm_sym_free(g);
+    }
     dev_free_all(g);
     delete g;
     return GR_OK;
@@ -113,10 +117,39 @@ gr_status gr_graph_info_get(const gr_graph *h, gr_graph_info *out) {
     return GR_OK;
 }
 
+gr_status pbfs_collective(Graph *g, int64_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts &o);
+
+static gr_status check_bfs_opts(const gr_bfs_opts &o) {
+    if (o.direction < 0 || o.direction > 2 || o.strategy < 0 || o.strategy > 2 || o.switch_rule < 0 ||
+        o.switch_rule > 1 || o.idempotent < 0 || o.idempotent > 1 || o.alpha < 0 || o.beta < 0) {
+        set_error("invalid gr_bfs_opts");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    return GR_OK;
+}
+
+// gr_bfs on a graph of gr_graph_create_partitioned: src is a GLOBAL id, the
+// outputs cover the owned block; collective over the comm's ranks (pbfs.cu)
+static gr_status pbfs_entry(Graph *g, int32_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts *opts) {
+    if (!depth_out) { set_error("depth_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
+    if (src < 0 || src >= g->n_global) {
+        set_error("src=%d not in [0, n=%lld)", src, (long long)g->n_global);
+        return GR_ERR_OUT_OF_RANGE;
+    }
+    gr_bfs_opts o = opts ? *opts : gr_bfs_opts{};
+    gr_status st = check_bfs_opts(o);
+    if (st != GR_OK) return st;
+    return pbfs_collective(g, src, depth_out, pred_out, o);
+}
+
 static gr_status bfs_args(gr_graph *h, int32_t src, const int32_t *depth_out, const gr_bfs_opts *opts,
                           gr_bfs_opts *o) {
     if (!h || !depth_out) { set_error("graph or depth_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     Graph *g = (Graph *)h;
+    if (g->part) {  // a gr_graph_create_part handle: global column ids, local rows
+        set_error("gr_bfs on a step-level partition (gr_graph_create_part); use gr_part_bfs_*");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
     if (src < 0 || src >= g->n) {
         set_error("src=%d not in [0, n=%lld)", src, (long long)g->n);
         return GR_ERR_OUT_OF_RANGE;
@@ -137,6 +170,7 @@ gr_status gr_graph_sync(gr_graph *h);
 gr_status gr_bfs(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts *opts) {
     g_err[0] = 0;
     gr_bfs_opts o;
+    if (h && ((Graph *)h)->comm) return pbfs_entry((Graph *)h, src, depth_out, pred_out, opts);
     gr_status st = bfs_args(h, src, depth_out, opts, &o);
     if (st != GR_OK) return st;
     Graph *g = (Graph *)h;
@@ -160,6 +194,7 @@ gr_status gr_bfs(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out
         GR_CUDA(cudaMemcpyAsync(pred_out, pred, g->n * sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
     g->last_launches = launches;
     g->last_delta = 0;
+    g->last_kind = 1; g->last_src = src; g->reached = -2;
     st = finish_run(g);
     if (st == GR_ERR_OVERFLOW && o.idempotent) {
         // the idempotent queue outgrew its capacity: redo with exactly-once claims
@@ -178,6 +213,10 @@ gr_status gr_bfs(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out
 gr_status gr_bfs_async(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pred_out,
                        const gr_bfs_opts *opts) {
     g_err[0] = 0;
+    if (h && ((Graph *)h)->comm) {
+        set_error("gr_bfs_async: a partitioned graph runs collective synchronous gr_bfs calls");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
     gr_bfs_opts o;
     gr_status st = bfs_args(h, src, depth_out, opts, &o);
     if (st != GR_OK) return st;
@@ -191,6 +230,7 @@ gr_status gr_bfs_async(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pr
     GR_CUDA(cudaGetLastError());
     g->last_launches = launches;
     g->last_delta = 0;
+    g->last_kind = 1; g->last_src = src; g->reached = -2;
     g->pending++;
     g->pending_kind = 1;
     g->pending_src = src;
@@ -204,6 +244,10 @@ static gr_status sssp_args(gr_graph *h, int32_t src, const uint32_t *dist_out, c
                            uint64_t *delta_out) {
     if (!h || !dist_out) { set_error("graph or dist_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     Graph *g = (Graph *)h;
+    if (g->part) {
+        set_error("gr_sssp on a step-level partition (gr_graph_create_part); use gr_part_sssp_*");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
     if (!g->has_w) { set_error("graph was created without weights"); return GR_ERR_NO_WEIGHTS; }
     if (src < 0 || src >= g->n) {
         set_error("src=%d not in [0, n=%lld)", src, (long long)g->n);
@@ -268,6 +312,7 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
         GR_CUDA(cudaMemcpyAsync(pred_out, pred, g->n * sizeof(int32_t), cudaMemcpyDeviceToHost, g->stream));
     g->last_launches = launches;
     g->last_delta = (uint32_t)(delta > 0xFFFFFFFFull ? 0xFFFFFFFFull : delta);
+    g->last_kind = 2; g->last_src = src; g->reached = -2;
     return finish_run(g);
 }
 
@@ -287,6 +332,7 @@ gr_status gr_sssp_async(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *p
     GR_CUDA(cudaGetLastError());
     g->last_launches = launches;
     g->last_delta = (uint32_t)(delta > 0xFFFFFFFFull ? 0xFFFFFFFFull : delta);
+    g->last_kind = 2; g->last_src = src; g->reached = -2;
     g->pending++;
     g->pending_kind = 2;
     g->pending_src = src;
@@ -338,7 +384,12 @@ gr_status gr_get_run_stats(gr_graph *h, gr_run_stats *out) {
     out->num_levels = g->stats_levels;
     out->num_records = g->stats_records;
     out->levels = g->stats_host;
-    out->reached = -1;
+    if (g->reached == -2) {  // first query since the run: count from the run's state
+        gr_status st = count_reached(g, &g->reached, &g->reached_edges);
+        if (st != GR_OK) return st;
+    }
+    out->reached = g->reached;
+    out->reached_edges = g->reached_edges;
     out->delta = g->last_delta;
     out->kernel_launches = g->last_launches;
     return GR_OK;

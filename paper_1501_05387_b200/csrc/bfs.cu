@@ -20,7 +20,7 @@
 // Control words every block needs (frontier size, counters) are read by one
 // thread per CTA and broadcast through shared memory: thousands of warps
 // reading one L2 address serialise on its slice.
-#include "frontier.cuh"
+#include "pull.cuh"
 
 namespace gr {
 
@@ -36,16 +36,6 @@ constexpr int64_t kSmallE = 16384;  // small mode: max frontier edges
 constexpr int kBfsStages = GR_BFS_STAGES;  // cp.async pipeline depth of the grid push advance (0: off)
 constexpr int kSmallCntBits = 24;   // count field of the small-mode packed counter
 constexpr unsigned long long kSmallCntMask = (1ull << kSmallCntBits) - 1;
-
-constexpr int kPullList = 96;   // pull: per-warp candidate list (< 64 + 32 before a batch)
-#ifndef GR_PULL_GRAB
-#define GR_PULL_GRAB 4
-#endif
-constexpr int kPullGrab = GR_PULL_GRAB;  // pull: bitmap words per grab
-#ifndef GR_PULL_LONG
-#define GR_PULL_LONG 4
-#endif
-constexpr int64_t kPullLong = GR_PULL_LONG;  // pull: longer unresolved in-lists are scanned by the warp
 
 struct BfsArgs {
     int64_t n, m;
@@ -274,211 +264,13 @@ struct SmallPushOp {
     }
 };
 
-// ---------------------------------------------------------------------------
-// Pull (bottom-up) step over in-edges: "pull starts with a
-// frontier of unvisited vertices, generating the new frontier by filtering
-// the unvisited frontier for vertices that have neighbors in the current
-// frontier"; the current frontier is held as a bitmap.
-// B200 design: each CTA owns a contiguous range of visited-bitmap words; its
-// warps take 16 words at a time and COMPACT the unvisited vertices of those
-// words into a per-warp shared-memory list (filter of the unvisited set, one
-// ballot per round), so every lane of a batch works on a real candidate (a
-// late pull step has ~1 candidate per 10 vertices: a lane-per-vertex sweep
-// would leave 90% of the lanes idle through the whole dependent chain
-// R' -> C' -> frontier bit). A batch is 64 candidates, two per lane, with
-// the loads of both issued back to back. Each candidate stops at its first
-// in-neighbour in the frontier (early exit; in-lists are ordered by neighbour
-// degree, so hubs come first). Found vertices set their bits in the next
-// frontier and visited bitmaps with fire-and-forget RED.OR.
-// The next frontier is kept as a bitmap only ("lazy queue"): the step counts
-// its size and edges (for the direction rule) and a following push step
-// builds the queue from the bitmap (bitmap_to_queue), so pull -> pull
-// sequences never write a queue.
-// ---------------------------------------------------------------------------
-
-struct PullCounts {
-    unsigned long long ndisc = 0, insp = 0, qcnt = 0, qedges = 0;
-    unsigned dmax = 0;
-};
-
-__device__ __forceinline__ void pull_level(const BfsArgs &a, const uint32_t *__restrict__ fcur,
-                                           uint32_t *__restrict__ fnext, int32_t next_depth, int *swork,
-                                           int32_t *wl, PullCounts &pc, uint32_t sbm, int64_t sbits) {
-    const int64_t nwords = (a.n + 31) / 32;
-    const int64_t wb0 = nwords * blockIdx.x / gridDim.x;
-    const int64_t wb1 = nwords * (blockIdx.x + 1) / gridDim.x;
-    const unsigned l = lane_id();
-    const unsigned long long pol = policy_evict_first();
-    const bool sym = a.Rt == a.R;
-    const uint32_t tail = (a.n & 31) ? ((1u << (a.n & 31)) - 1u) : 0xffffffffu;
-    auto fbit = [&](int32_t u) -> bool {
-        const uint32_t fw = u < sbits ? lds_u32(sbm + 4u * (uint32_t)(u >> 5)) : __ldg(fcur + (u >> 5));
-        return (fw >> (u & 31)) & 1u;
-    };
-    int cnt = 0;  // warp-uniform
-    auto process = [&](int k) {  // candidates wl[0, k), k <= 64
-        int32_t v[2], par[2], u0[2];
-        int64_t beg[2], end[2];
-        bool fnd[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) v[q] = ((int)l + 32 * q < k) ? wl[l + 32 * q] : -1;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            beg[q] = v[q] >= 0 ? a.Rt[v[q]] : 0;
-            end[q] = v[q] >= 0 ? a.Rt[v[q] + 1] : 0;
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Ct + beg[q], pol) : -1;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            fnd[q] = u0[q] >= 0 && fbit(u0[q]);
-            par[q] = u0[q];
-            pc.insp += (u0[q] >= 0);
-        }
-        // the rest of each unresolved list: first by its lane (4 edges a step,
-        // at most kPullLong edges), then what is left of the long ones by the
-        // whole warp, 32 edges a step with a ballot early exit (one lane
-        // scanning a long list alone held its warp for 100+ us on C3)
-        int64_t nxt[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            nxt[q] = beg[q] + 1;
-            if (fnd[q]) continue;
-            const int64_t lim = (end[q] - nxt[q] > kPullLong) ? nxt[q] + kPullLong : end[q];
-            for (int64_t e = nxt[q]; e < lim && !fnd[q]; e += 4) {
-                int32_t u[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) u[j] = (e + j < lim) ? ld_stream(a.Ct + e + j, pol) : -1;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    if (!fnd[q] && u[j] >= 0) {
-                        ++pc.insp;
-                        if (fbit(u[j])) { fnd[q] = true; par[q] = u[j]; }
-                    }
-                }
-            }
-            nxt[q] = lim;
-        }
-        bool lng[2];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) lng[q] = !fnd[q] && nxt[q] < end[q];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            unsigned lm = __ballot_sync(0xffffffffu, lng[q]);
-            while (lm) {
-                const int ld = __ffs(lm) - 1;
-                lm &= lm - 1;
-                const int64_t b = __shfl_sync(0xffffffffu, nxt[q], ld);
-                const int64_t e = __shfl_sync(0xffffffffu, end[q], ld);
-                int32_t hitu = -1;
-                for (int64_t x = b; x < e; x += 32) {
-                    const int32_t u = (x + l < e) ? ld_stream(a.Ct + x + l, pol) : -1;
-                    const bool hit = u >= 0 && fbit(u);
-                    const unsigned bm = __ballot_sync(0xffffffffu, hit);
-                    const int first = bm ? __ffs(bm) - 1 : 32;
-                    pc.insp += (u >= 0 && (int)l <= first);
-                    if (bm) {
-                        hitu = __shfl_sync(0xffffffffu, u, first);
-                        break;
-                    }
-                }
-                if ((int)l == ld && hitu >= 0) { fnd[q] = true; par[q] = hitu; }
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            if (!fnd[q]) continue;
-            const int32_t x = v[q];
-            a.depth[x] = next_depth;
-            if (a.pred) a.pred[x] = par[q];
-            const uint32_t bit = 1u << (x & 31);
-            atomicOr(fnext + (x >> 5), bit);      // RED.OR
-            atomicOr(a.visited + (x >> 5), bit);  // RED.OR
-            const int64_t deg = sym ? end[q] - beg[q] : a.R[x + 1] - a.R[x];
-            ++pc.ndisc;
-            if (deg > 0) {
-                ++pc.qcnt;
-                pc.qedges += (unsigned long long)deg;
-                pc.dmax = max(pc.dmax, (unsigned)deg);
-            }
-        }
-        // keep the unprocessed tail (cnt - k < 32 entries) at the front
-        __syncwarp();
-        const int rem = cnt - k;
-        const int32_t t = ((int)l < rem) ? wl[k + l] : 0;
-        __syncwarp();
-        if ((int)l < rem) wl[l] = t;
-        __syncwarp();
-        cnt = rem;
-    };
-    for (;;) {
-        int c = 0;
-        if (l == 0) c = atomicAdd(swork, kPullGrab);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        const int64_t w0 = wb0 + c;
-        if (w0 >= wb1) break;
-        const int64_t wi = w0 + l;
-        uint32_t cm = ((int)l < kPullGrab && wi < wb1) ? ~a.visited[wi] : 0u;
-        if (wi == nwords - 1) cm &= tail;
-        // word by word, lane b takes bit b: the list stays sorted by vertex id,
-        // so a batch's depth/pred stores and bitmap REDs touch few lines
-        unsigned nz = __ballot_sync(0xffffffffu, cm != 0);
-        while (nz) {
-            const int j = __ffs(nz) - 1;
-            nz &= nz - 1;
-            const uint32_t w = __shfl_sync(0xffffffffu, cm, j);
-            if ((w >> l) & 1u) wl[cnt + __popc(w & lanemask_lt())] = (int32_t)((w0 + j) * 32 + l);
-            cnt += __popc(w);
-            __syncwarp();
-            if (cnt >= 64) process(64);
-        }
-    }
-    while (cnt > 0) process(cnt < 64 ? cnt : 64);
-}
-
-// Frontier bitmap -> queue (the other direction of the
-// conversion): the frontier of a pull step, needed as a queue when the next
-// step pushes. Warp-strided over 32-word chunks; appends (v, degree prefix,
-// R[v]) for every set bit with out-degree > 0.
-template <class App>
-__device__ __forceinline__ void bitmap_to_queue(const BfsArgs &a, const uint32_t *__restrict__ fb,
-                                                int64_t gw, int64_t nw, App &app) {
-    const int64_t nwords = (a.n + 31) / 32;
-    const unsigned l = lane_id();
-    for (int64_t w0 = gw * 32; w0 < nwords; w0 += nw * 32) {
-        const int64_t wi = w0 + l;
-        uint32_t bits = wi < nwords ? __ldcg(fb + wi) : 0u;
-        while (__any_sync(0xffffffffu, bits != 0)) {
-            const bool has = bits != 0;
-            int32_t v = 0;
-            int64_t rs = 0, deg = 0;
-            if (has) {
-                v = (int32_t)(wi * 32 + (__ffs(bits) - 1));
-                bits &= bits - 1;
-                rs = a.R[v];
-                deg = a.R[v + 1] - rs;
-            }
-            app.push(has && deg > 0, v, deg, rs);
-        }
-    }
-    app.finish();
-}
-
-// Direction decision (reading A-3). Pure function of counters
-// every block reads after the same barrier, so all blocks agree.
+// Direction decision (reading A-3): direction_rule (pull.cuh) on
+// counters every block reads after the same barrier, so all blocks agree.
 __device__ __forceinline__ int decide_direction(const BfsArgs &a, int dir, int64_t f, int64_t mf,
                                                 int64_t u_cnt, int64_t m_u, int64_t prev_f,
                                                 int64_t nwords) {
-    if (a.direction != 0) return a.direction;
-    if (a.switch_rule == 1) return (u_cnt < f) ? 2 : 1;  // paper-literal: unvisited < frontier
-    if (dir == 1) {
-        // Beamer: pull when the frontier's edges exceed the unvisited edges / alpha;
-        // plus: a pull step sweeps every bitmap word, so require m_f >= n/32.
-        if ((double)mf > (double)m_u / a.alpha && mf >= nwords) return 2;
-        return 1;
-    }
-    if ((double)f < (double)a.nonisolated / a.beta && f < prev_f) return 1;
-    return 2;
+    return direction_rule(a.direction, a.switch_rule, a.alpha, a.beta, a.nonisolated, dir, f, mf, u_cnt, m_u,
+                          prev_f, nwords);
 }
 
 struct BfsState {  // per-traversal heuristic state, identical in every CTA
@@ -833,7 +625,8 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
                 grid.sync();
             }
             PullCounts pc;
-            pull_level(a, fb_c, fb_n, L + 1, &s->work, s->u.plist[wib], pc, sbm, snap ? sbits : 0);
+            pull_level(a, fb_c, fb_n, L + 1, &s->work, s->u.plist[wib], pc, sbm, snap ? sbits : 0,
+                       nwords * blockIdx.x / gridDim.x, nwords * (blockIdx.x + 1) / gridDim.x);
             ndisc = pc.ndisc;
             insp = pc.insp;
             // lazy queue: only the size, edges and max degree of the next frontier

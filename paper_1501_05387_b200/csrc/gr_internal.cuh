@@ -30,6 +30,7 @@ constexpr int kWarpsPerBlock = kBlock / kWarp;
 constexpr int kStageCap = GR_STAGE_CAP;  // per-warp smem staging of appended vertices
 constexpr int kMaxStatRecords = 1 << 16; // per-level records kept for gr_get_run_stats
 constexpr int kSlots = 4;                // rotating per-level control slots
+constexpr int kMaxRanks = 8;             // one NVSwitch box: 1/2/4/8 GPUs (north star)
 
 // ---------------------------------------------------------------- error plumbing
 void set_error(const char *fmt, ...);
@@ -67,7 +68,38 @@ struct Ctl {
     unsigned long long far_count[2];
     long long bstate[8];           // small-mode handoff of the traversal state
     unsigned long long sticky;     // some run since the last gr_graph_sync overflowed
+    unsigned long long epoch;      // partitioned runs: cross-rank barrier epochs used so far
 };
+
+struct Graph;
+struct LoopGroup;
+// gr_comm: one rank of a multi-GPU group (comm.cu). Either a real rank (one
+// process per GPU, the library's own ncclComm_t used for the collective
+// set-up steps: IPC handle and degree all-gathers) or one virtual rank of a
+// loopback group (all ranks in one process on one GPU; the partitioned kernel
+// then hosts every rank in one cooperative launch -- the test harness for the
+// multi-rank logic on a single GPU).
+struct Comm {
+    int rank = 0, nranks = 1, device = 0;
+    void *nccl = nullptr;          // ncclComm_t (real ranks)
+    LoopGroup *group = nullptr;    // loopback ranks
+};
+struct LoopGroup {
+    int P = 0, device = 0, alive = 0;
+    Comm *ranks[kMaxRanks] = {};
+    Graph *graphs[kMaxRanks] = {};
+    // a collective call (gr_bfs / gr_sssp) joined by some ranks, launched when all have
+    int joined = 0;                // bitmask of ranks that joined
+    int kind = 0;                  // 1 BFS, 2 SSSP
+    int64_t src = 0;
+    void *out0[kMaxRanks] = {}, *out1[kMaxRanks] = {};
+    gr_bfs_opts bopts{};
+    gr_sssp_opts sopts{};
+};
+gr_status nccl_fail(int res, const char *what);
+gr_status comm_allgather_bytes(Comm *c, const void *dsend, void *drecv, size_t bytes, cudaStream_t s);
+gr_status comm_sym_alloc(Comm *c, Graph *g, size_t bytes);
+void comm_sym_free(Graph *g);
 
 // ---------------------------------------------------------------- graph object
 struct Graph {
@@ -107,7 +139,9 @@ struct Graph {
     gr_level_stats *stats_dev = nullptr;
     gr_level_stats *stats_host = nullptr;
     int stats_levels = 0, stats_records = 0;
-    int64_t reached = 0;
+    int64_t reached = -1, reached_edges = -1;  // totals of the last run (lazy, gr_get_run_stats)
+    int last_kind = 0;             // 1 BFS, 2 SSSP: the kind of the last single-GPU run
+    int32_t last_src = 0;
     uint32_t last_delta = 0;
     int last_launches = 0;
     int64_t bytes = 0;
@@ -133,6 +167,16 @@ struct Graph {
     int32_t *part_depth = nullptr, *part_pred = nullptr;
     uint32_t *pull_shard = nullptr;   // [block/32] frontier shard written by the last pull step
     int32_t pull_shard_level = -1;     // the level whose frontier pull_shard holds (-1: none)
+    // partitioned graph of a gr_comm (gr_graph_create_partitioned; pbfs.cu)
+    Comm *comm = nullptr;
+    char *sym = nullptr;               // symmetric region (same layout on every rank)
+    size_t sym_bytes = 0;
+    char *sym_peer[kMaxRanks] = {};    // every rank's region, mapped here (sym_peer[rank] = sym)
+    bool sym_ipc[kMaxRanks] = {};      // sym_peer[q] was opened with cudaIpcOpenMemHandle
+    bool prepared = false;             // peers mapped, pull lists ordered by global degree
+    bool flags_keep_order = false;     // GR_KEEP_ORDER: keep the caller's pull-list order
+    void *pbfs_ranks = nullptr;        // device table of the ranks a launch hosts (pbfs.cu PRank)
+    int64_t m_global = 0, nonisolated_global = 0;
     // partitioned SSSP (partition_sssp.cu)
     unsigned long long *ps_best = nullptr;  // [n_global] best (dist<<32|pred) shipped per remote vertex
     int32_t *ps_sstamp = nullptr;           // [n_global] step of the last shipment (one per step)
@@ -153,6 +197,7 @@ struct Graph {
 };
 
 gr_status dev_alloc(Graph *g, void **p, size_t bytes);
+gr_status count_reached(Graph *g, int64_t *reached, int64_t *reached_edges);
 void dev_free_all(Graph *g);
 
 // ---------------------------------------------------------------- device helpers

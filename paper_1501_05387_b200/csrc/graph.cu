@@ -34,6 +34,57 @@ void dev_free_all(Graph *g) {
     if (g->stats_host) cudaFreeHost(g->stats_host);
 }
 
+// ---------------------------------------------------------------- run totals
+// Vertices reached by the last run and the directed edges leaving them (the
+// TEPS numerator m_reached, reading A-14), from the run's internal state: the
+// visited bitmap of a BFS (every discovery sets its bit; in-degree-0 vertices
+// are pre-set from `noin` and only count if they are the source) or the
+// packed dist|pred array of an SSSP (dist != UINT32_MAX). Launched by
+// gr_get_run_stats, outside any timed region.
+__global__ void reached_kernel(int kind, const uint32_t *visited, const uint32_t *noin,
+                               const unsigned long long *dp, const int64_t *R, int64_t n, int32_t src,
+                               unsigned long long *out) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long cnt = 0, edges = 0;
+    for (int64_t v = tid; v < n; v += nt) {
+        bool r;
+        if (kind == 1) {
+            const uint32_t bit = 1u << (v & 31);
+            r = (visited[v >> 5] & bit) && (!(noin[v >> 5] & bit) || v == src);
+        } else {
+            r = (dp[v] >> 32) != 0xFFFFFFFFull;
+        }
+        if (r) { ++cnt; edges += (unsigned long long)(R[v + 1] - R[v]); }
+    }
+    cnt = warp_sum(cnt);
+    edges = warp_sum(edges);
+    if ((threadIdx.x & 31) == 0 && (cnt || edges)) {
+        atomicAdd(out, cnt);
+        atomicAdd(out + 1, edges);
+    }
+}
+
+gr_status count_reached(Graph *g, int64_t *reached, int64_t *reached_edges) {
+    *reached = -1;
+    *reached_edges = -1;
+    if (g->last_kind == 0 || g->part) return GR_OK;
+    if (g->last_kind == 2 && !g->dp) return GR_OK;
+    unsigned long long *d = nullptr;
+    GR_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));
+    GR_CUDA(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), g->stream));
+    const int64_t blocks = (g->n + 255) / 256 < 4096 ? (g->n + 255) / 256 : 4096;
+    reached_kernel<<<(unsigned)blocks, 256, 0, g->stream>>>(g->last_kind, g->visited, g->noin, g->dp, g->R,
+                                                             g->n, g->last_src, d);
+    unsigned long long h[2] = {0, 0};
+    GR_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, g->stream));
+    GR_CUDA(cudaStreamSynchronize(g->stream));
+    cudaFree(d);
+    *reached = (int64_t)h[0];
+    *reached_edges = (int64_t)h[1];
+    return GR_OK;
+}
+
 // ---------------------------------------------------------------- validation
 // err[0] = first bad row-offset index (or INT64_MAX), err[1] = first bad edge.
 __global__ void validate_kernel(const int64_t *R, const int32_t *C, int64_t n, int64_t m,

@@ -1,12 +1,11 @@
 """Parity at BASELINE.json's full sizes, in the launch configuration bench.py
 times (same kernels, same default options).
 
-C1-C4: element-by-element against the CPU oracle (BFS is seconds; Dijkstra
-on C3/C4 tens of seconds, so one source). C5 (1.05B edges): the O(m)
-BFS certificate evaluated on the GPU with plain torch ops in this test
-(a property that decides exactness at any size), plus the
-oracle on sampled sources is too slow for the host, so depths of a sample of
-vertices are re-derived by the certificate only.
+Every config, C1-C5, element by element against the CPU oracle (BFS is
+seconds per source, ~6 s on C5's 1.05B edges; Dijkstra on C3/C4 tens of
+seconds, so one source), plus the oracle's O(m) certificate on the parents.
+C5 is also run 1D-partitioned (the configuration it is defined on, SURVEY
+§8(e)): 8 partitions in one process and a world-size-1 NCCL group.
 """
 import numpy as np
 import pytest
@@ -64,52 +63,97 @@ def test_c4_road_bfs_sssp(gr):
     assert np.array_equal(got, ref), int((got != ref).sum())
 
 
-def _bfs_certificate_torch(R, C, src, depth, pred):
-    """BFS certificate (oracle.check_bfs) restated with torch ops so it runs
-    on the GPU at 1B edges: (i) src only depth 0; (ii) depth[v] <= depth[u]+1
-    along every edge from a reached u, v reached; (iii) pred edge exists and
-    drops depth by one; (iv) -1 <=> -1."""
-    n = R.numel() - 1
-    assert int(depth[src]) == 0 and int((depth == 0).sum()) == 1
-    deg = R[1:] - R[:-1]
-    m = C.numel()
-    chunk = 1 << 27
-    s = 0
-    src_of = None
-    for e0 in range(0, m, chunk):
-        e1 = min(m, e0 + chunk)
-        u = torch.searchsorted(R, torch.arange(e0, e1, device=R.device), right=True) - 1
-        du = depth[u]
-        dv = depth[C[e0:e1].long()]
-        live = du >= 0
-        assert not bool((live & ((dv < 0) | (dv > du + 1))).any())
-    assert bool(((depth == -1) == (pred == -1)).all())
-    assert int(pred[src]) == src
-    reached = torch.nonzero(depth > 0).squeeze(1)
-    p = pred[reached].long()
-    assert bool((depth[p] == depth[reached] - 1).all())
-    # (pred[v], v) in E: binary search v in the sorted list of p
-    lo = R[p]
-    hi = R[p + 1]
-    for _ in range(40):
-        mid = (lo + hi) // 2
-        go = C[torch.clamp(mid, max=m - 1)].long() < reached
-        lo = torch.where(go & (mid < hi), mid + 1, lo)
-        hi = torch.where(go & (mid < hi), hi, mid)
-    assert bool((C[torch.clamp(lo, max=m - 1)].long() == reached).all())
+def test_c2_kron21_bfs_variants(gr):
+    """The idempotent (atomic-free) discovery and the paper-literal switch
+    rule (A-3, A-5, A-6) at C2's full size, bit-exact against the oracle."""
+    g = gg.make_config("c2_kron21", device="cuda")
+    G = gr.Graph(g.R, g.C, None, symmetric=True)
+    R, C, _ = g.numpy()
+    for s in gg.sources(g, 2):
+        ref, _ = oracle.bfs(R, C, s, want_pred=False)
+        for kw in (dict(idempotent=True), dict(switch_rule=1), dict(idempotent=True, direction="push"),
+                   dict(direction="pull")):
+            depth, pred = G.bfs(s, **kw)
+            got = depth.cpu().numpy()
+            assert np.array_equal(got, ref), (s, kw, int((got != ref).sum()))
+            assert oracle.check_bfs(R, C, s, got, pred.cpu().numpy()) == [], (s, kw)
+    G.close()
 
 
-def test_c5_kron25_bfs_certificate(gr):
+def test_c5_kron25_bfs(gr):
+    """C5 (Kronecker scale 25, ~1.05B directed edges) single-GPU BFS, auto and
+    push, element by element against the oracle's FIFO BFS (~6 s per source
+    on one host core), plus the certificate on the parents; the run totals of
+    gr_get_run_stats (reached, reached_edges) against the oracle's."""
     g = gg.make_config("c5_kron25", device="cuda")
     G = gr.Graph(g.R, g.C, None, symmetric=True)
-    srcs = gg.sources(g, 2)
-    for s in srcs:
-        depths = []
+    R, C, _ = g.numpy()
+    for s in gg.sources(g, 2):
+        ref, _ = oracle.bfs(R, C, s, want_pred=False)
         for d in ("auto", "push"):
             depth, pred = G.bfs(s, direction=d)
-            _bfs_certificate_torch(g.R, g.C, s, depth, pred)
-            depths.append(depth)
-        assert torch.equal(depths[0], depths[1])
+            got = depth.cpu().numpy()
+            assert np.array_equal(got, ref), (s, d, int((got != ref).sum()))
+            assert oracle.check_bfs(R, C, s, got, pred.cpu().numpy()) == [], (s, d)
+            st = G.run_stats()
+            assert st["reached"] == int((ref >= 0).sum())
+            assert st["reached_edges"] == oracle.reached_edges(R, ref, -1)
+    G.close()
+
+
+def test_c5_kron25_bfs_partitioned(gr):
+    """The 1D-partitioned BFS on the full C5 graph: P = 8
+    partitions in one process (device-copy exchange) and a world-size-1 NCCL
+    group, bit-exact against the oracle."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+    from paper_1501_05387_b200 import dist as grd
+    g = gg.make_config("c5_kron25", device="cuda")
+    R, C, _ = g.numpy()
+    s = gg.sources(g, 1)[0]
+    ref, _ = oracle.bfs(R, C, s, want_pred=False)
+    P = 8
+    deg_global = (g.R[1:] - g.R[:-1]).to(torch.int32)
+    parts = []
+    for r in range(P):
+        v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, P, r)
+        parts.append(grd.GpuPartition(Rl, Cl, g.n, P, r))
+        parts[-1].order_pull_lists(deg_global)
+        del Rl, Cl
+    grp = grd.LoopbackGroup(parts)
+    depths = [torch.empty(pt.n_local, dtype=torch.int32, device="cuda") for pt in parts]
+    preds = [torch.empty(pt.n_local, dtype=torch.int32, device="cuda") for pt in parts]
+    grp.bfs(s, depths, preds, direction="auto")
+    got = torch.cat(depths).cpu().numpy()
+    assert np.array_equal(got, ref), int((got != ref).sum())
+    assert oracle.check_bfs(R, C, s, got, torch.cat(preds).cpu().numpy()) == []
+    for pt in parts:
+        pt.close()
+    del parts, depths, preds
+    torch.cuda.empty_cache()
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(sk.getsockname()[1])
+    sk.close()
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, 1, 0)
+        part = grd.GpuPartition(Rl, Cl, g.n, 1, 0)
+        del Rl, Cl
+        ex = grd.TorchDistExchange()
+        part.order_pull_lists(grd.global_degrees(part, ex))
+        depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        pred = torch.empty(g.n, dtype=torch.int32, device="cuda")
+        grd.bfs_partitioned(part, ex, s, depth, pred)
+        got = depth.cpu().numpy()
+        assert np.array_equal(got, ref), int((got != ref).sum())
+        assert oracle.check_bfs(R, C, s, got, pred.cpu().numpy()) == []
+        part.close()
+    finally:
+        dist.destroy_process_group()
 
 
 # ---- the paper's other primitives at full size (SURVEY §8(f) f3/f4) --------

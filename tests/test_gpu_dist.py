@@ -139,6 +139,12 @@ def test_part_errors(grd):
                                         4, 0, None, ctypes.byref(h))  # rank 0 does not own [v0, v1)
     assert st == 1 and "must own" in gr.gr_last_error()
     pt = grd.GpuPartition(Rc, Cc, g.n, 2, 1)
+    # the single-GPU entry points must refuse a step-level partition handle
+    # (its columns are global ids: depth/visited would be indexed out of range)
+    dd = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    assert gr.load().gr_bfs(pt.handle, 0, dd.data_ptr(), None, None) == 1
+    assert "partition" in gr.gr_last_error()
+    assert gr.load().gr_sssp(pt.handle, 0, dd.data_ptr(), None, None) == 1
     d = torch.empty(pt.n_local, dtype=torch.int32)  # host memory: rejected
     with pytest.raises(gr.GrError):
         pt.begin(0, d, None)

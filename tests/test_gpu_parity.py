@@ -239,6 +239,24 @@ def test_run_stats_levels(gr):
         want = int(((ref == L) & (deg > 0)).sum())
         assert rec["frontier"] == want
         assert rec["frontier_edges"] == int(deg[ref == L].sum())
+    # run totals: vertices reached and the TEPS numerator (A-14)
+    assert st["reached"] == int((ref >= 0).sum())
+    assert st["reached_edges"] == oracle.reached_edges(R, ref, -1)
+    gw = gg.assign_weights(gg.make_config("c1_rmat16"), seed=2)
+    Gw = _dev(gw, gr)
+    Rw, Cw, Ww = gw.numpy()
+    s = gg.sources(gw, 1)[0]
+    Gw.sssp(s)
+    dref, _ = oracle.sssp(Rw, Cw, Ww, s)
+    st = Gw.run_stats()
+    assert st["reached"] == int((dref != oracle.UINT32_MAX).sum())
+    assert st["reached_edges"] == oracle.reached_edges(Rw, dref, oracle.UINT32_MAX)
+    # idempotent discovery (duplicates possible in the queue): totals stay exact
+    G.bfs(s, direction="auto", idempotent=True)
+    dref2, _ = oracle.bfs(R, C, s)
+    st = G.run_stats()
+    assert st["reached"] == int((dref2 >= 0).sum())
+    assert st["reached_edges"] == oracle.reached_edges(R, dref2, -1)
 
 
 @pytest.mark.parametrize("strategy", ["twc", "lb"])

@@ -374,3 +374,68 @@ def test_table3_teps_arithmetic():
     for r in rows:
         mteps = teps(r["edges_M"] * 1e6, r["ms"] * 1e-3) / 1e6
         assert abs(mteps - r["mteps"]) / r["mteps"] < 0.013, r
+
+
+def test_metrics_aggregates():
+    """Harmonic mean / median / Graph500 halving on values
+    whose results are fixed by arithmetic: 1 edge per second per source at
+    GTEPS 1, 2, 4 -> harmonic mean 3 / (1 + 1/2 + 1/4) = 12/7, median 2."""
+    from paper_1501_05387_b200 import metrics
+    edges = [1e9, 2e9, 4e9]
+    ms = [1000.0, 1000.0, 1000.0]
+    s = metrics.summarize(edges, ms)
+    assert abs(s["harmonic_mean"] - 12.0 / 7.0) < 1e-12
+    assert s["median"] == 2.0
+    assert abs(s["aggregate"] - 7.0 / 3.0) < 1e-12
+    assert abs(s["graph500_aggregate"] - 7.0 / 6.0) < 1e-12
+    assert metrics.harmonic_mean([5.0]) == 5.0
+
+
+# ---------------------------------------------------------------- reached_edges (TEPS numerator, A-14)
+
+def test_reached_edges_closed_forms():
+    """oracle.reached_edges = directed edges whose source is reached, checked
+    against counts fixed by the graph's shape: path P_n from anywhere reaches
+    all 2(n-1) directed edges; a disjoint union P_5 + K_4 reaches 8 edges from
+    the path and 4*3 = 12 from the clique; a directed chain 0->1->...->n-1
+    from vertex k reaches the n-1-k edges after it; an isolated source reaches
+    no edge."""
+    R, C, _ = gg.path(7).numpy()
+    d, _ = oracle.bfs(R, C, 3)
+    assert oracle.reached_edges(R, d, -1) == 12
+    g = gg.from_edges(9, [(0, 1), (1, 2), (2, 3), (3, 4)] +
+                      [(a, b) for a in range(5, 9) for b in range(a + 1, 9)])
+    R, C, _ = g.numpy()
+    assert oracle.reached_edges(R, oracle.bfs(R, C, 2)[0], -1) == 8
+    assert oracle.reached_edges(R, oracle.bfs(R, C, 6)[0], -1) == 12
+    n = 10
+    g = gg.from_edges(n, [(i, i + 1) for i in range(n - 1)], symmetrize=False)
+    R, C, _ = g.numpy()
+    for k in (0, 4, 9):
+        assert oracle.reached_edges(R, oracle.bfs(R, C, k)[0], -1) == n - 1 - k
+    g = gg.from_edges(4, [(1, 2), (2, 3)])
+    R, C, _ = g.numpy()
+    assert oracle.reached_edges(R, oracle.bfs(R, C, 0)[0], -1) == 0
+    # SSSP sentinel: unreached = UINT32_MAX
+    gw = gg.assign_weights(gg.from_edges(6, [(0, 1), (1, 2), (3, 4)]), seed=1)
+    R, C, W = gw.numpy()
+    dist, _ = oracle.sssp(R, C, W, 0)
+    assert oracle.reached_edges(R, dist, INF) == 4
+
+
+def test_reached_edges_brute_force():
+    """Against an explicit edge-list count on random small graphs: for every
+    (u, v) in the edge list, count it iff u is reachable from s (reachability
+    by scipy's breadth_first_order, a library routine)."""
+    for seed in range(6):
+        g = gg.directed_random(300, 900, seed=seed) if seed % 2 else gg.erdos_renyi(300, 400, seed=seed)
+        R, C, _ = g.numpy()
+        n = len(R) - 1
+        A = sp.csr_matrix((np.ones(len(C)), C, R), shape=(n, n))
+        for s in (0, 17, 150):
+            order = csgraph.breadth_first_order(A, s, directed=True, return_predecessors=False)
+            reach = np.zeros(n, bool)
+            reach[order] = True
+            src_of = np.repeat(np.arange(n), np.diff(R))
+            want = int(reach[src_of].sum())
+            assert oracle.reached_edges(R, oracle.bfs(R, C, s)[0], -1) == want
