@@ -75,9 +75,15 @@ def parse():
     ap.add_argument("--keep-order", action="store_true",
                     help="partitioned BFS: keep the caller's pull-list order (no gr_part_order_pull_lists)")
     ap.add_argument("--partitioned", action="store_true",
-                    help="1D-partitioned BFS / SSSP over all ranks (NCCL exchange per step); "
-                         "default graph c5_kron25 (BFS) / c3_orkut (SSSP)")
+                    help="1D-partitioned BFS / SSSP over all ranks; default graph c5_kron25 (BFS) / "
+                         "c3_orkut (SSSP). The default for --gpus N > 1 (BASELINE config 5)")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent replicas of the single-GPU run (sources sharded) instead "
+                         "of the 1D-partitioned config-5 run")
     a = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "0")) or a.gpus
+    if world > 1 and not a.replicas and a.prim in ("bfs", "sssp"):
+        a.partitioned = True
     if a.partitioned and a.config == "c2_kron21" and "--config" not in sys.argv:
         a.config = "c3_orkut" if a.prim == "sssp" else "c5_kron25"
     return a
@@ -237,11 +243,172 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------- partitioned (multi-GPU) arm
 
-def run_partitioned(args, rank, world, dev):
-    """BFS over a 1D vertex partition of one graph across all ranks (SURVEY
-    §8(e)): strong scaling (the graph is fixed, each rank owns n/P vertices).
-    Each timed step = one full BFS; time = max over ranks of the CUDA-event
-    span of the step (the level loop synchronises with the host every level)."""
+NVLINK_PEER_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction per GPU (900 nominal)
+
+
+def partitioned_bytes(levels, n, nonisolated):
+    """SURVEY §8(d) algorithmic HBM bytes of one partitioned BFS, summed over
+    all ranks, from the global per-level records (the single-GPU model; u of
+    a pull level = non-isolated vertices not yet discovered)."""
+    B = 8 * n
+    found = 1
+    for r in levels:
+        f, mf, d, ins = r["frontier"], r["frontier_edges"], r["discovered"], r["inspected_edges"]
+        if r["direction"] == 1:
+            B += 12 * f + 4 * mf + 12 * d
+        else:
+            B += n / 8 + 8 * max(0, nonisolated - found) + 4 * ins + 8 * d + n / 8
+        found += d
+    return B
+
+
+def run_partitioned_bfs(args, rank, world, dev):
+    """BASELINE config 5: BFS over a 1D vertex partition of one graph across
+    all ranks through the library's own group
+    (gr_comm_create: NCCL communicator bootstrapped from a torch.distributed
+    broadcast of the unique id) and collective gr_bfs on
+    gr_graph_create_partitioned graphs: one persistent kernel per rank runs
+    every level, exchange included (peer-memory stores over NVLink). Strong
+    scaling: the graph is fixed, each rank owns n/P vertices. Each timed step
+    = one full BFS; time = max over ranks of the CUDA-event span of the call.
+    E(P) = GTEPS(P) / (P * GTEPS(1)), GTEPS(1) = rank 0's single-GPU kernel
+    (gr_bfs on the whole graph) on the same sources, measured in this run."""
+    import torch
+    import torch.distributed as dist
+
+    import graphgen as gg
+    import paper_1501_05387_b200 as gr
+    from paper_1501_05387_b200 import metrics
+    from paper_1501_05387_b200 import multigpu as mg
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29517")
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    g = gg.make_config(args.config, device=dev)
+    n, m = g.n, g.m
+    srcs = gg.sources(g, args.warmup + args.steps)
+    nonisolated = int((g.R[1:] > g.R[:-1]).sum())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    # single-GPU reference for E(P): rank 0, whole graph, same sources
+    single = None
+    if rank == 0 and not args.no_extras:
+        G = gr.Graph(g.R, g.C, None, symmetric=True)
+        d1 = torch.empty(n, dtype=torch.int32, device=dev)
+        for s in srcs[: args.warmup]:
+            G.bfs(s, d1, None)
+        e1s, ms1 = 0, 0.0
+        for s in srcs[args.warmup:]:
+            flush.zero_()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            G.bfs(s, d1, None)
+            a1.record()
+            torch.cuda.synchronize()
+            ms1 += a0.elapsed_time(a1)
+            e1s += G.run_stats()["reached_edges"]
+        single = metrics.gteps(e1s, ms1 * 1e-3)
+        G.close()
+        del d1
+    v0, v1, Rl, Cl, _ = mg.partition_csr(g.R, g.C, world, rank)
+    del g
+    torch.cuda.empty_cache()
+    comm = mg.Comm.from_torch(dev.index)
+    part = mg.PartitionedGraph(comm, Rl, Cl, n)
+    del Rl, Cl
+    torch.cuda.empty_cache()
+    depth = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
+    pred = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
+    for s in srcs[: args.warmup]:
+        part.bfs(s, depth, pred)
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = gr.gr_kernel_launch_count()
+    ms, edges, recs = [], [], []
+    with Clocks(dev.index) as clk:
+        for s in srcs[args.warmup:]:
+            flush.zero_()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            part.bfs(s, depth, pred)
+            e1.record()
+            torch.cuda.synchronize()
+            st = part.run_stats()
+            t = torch.tensor([e0.elapsed_time(e1), float(st["reached_edges"])], dtype=torch.float64, device=dev)
+            tm = t[:1].clone()
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            dist.all_reduce(t[1:])
+            ms.append(float(tm[0]))
+            edges.append(float(t[1]))
+            recs.append(st)
+    launches = gr.gr_kernel_launch_count() - launches0
+    # end to end through the C ABI: host (pinned) outputs, host wall clock, max over ranks
+    pin_d = torch.empty(v1 - v0, dtype=torch.int32, pin_memory=True)
+    pin_p = torch.empty(v1 - v0, dtype=torch.int32, pin_memory=True)
+    part.bfs(srcs[0], pin_d, pin_p)
+    e2e = []
+    for s in srcs[args.warmup:]:
+        dist.barrier()
+        t0 = time.perf_counter()
+        part.bfs(s, pin_d, pin_p)
+        t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e.append(float(t[0]))
+    dist.barrier()
+    if rank == 0:
+        summ = metrics.summarize(edges, ms)
+        value = summ["aggregate"]
+        peak, peak_src = load_peaks()
+        byts = [partitioned_bytes(r["levels"], n, nonisolated) for r in recs]
+        xbytes = [sum(l["aux"] for l in r["levels"]) for r in recs]
+        tot_s = sum(ms) * 1e-3
+        per_gpu = sum(byts) / world / tot_s / 1e9
+        nv = sum(xbytes) / world / tot_s / 1e9
+        lv = recs[-1]["levels"]
+        out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": sum(ms) / len(ms), "higher_is_better": True,
+               "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+               "config": {"workload": "%s bfs 1D-partitioned direction-optimizing, fused exchange over peer "
+                                      "memory (gr_comm + gr_graph_create_partitioned + collective gr_bfs)"
+                                      % args.config,
+                          "graph": CONFIG_DESC[args.config], "n": n, "m": m,
+                          "sources": "%d seeded sources with degree>=1 (S:519)" % args.steps,
+                          "parallelism": "1D vertex partition over %d rank(s), one persistent kernel per rank" % world,
+                          "l2": "flushed (256 MiB write) between timed steps"},
+               "throughput": summ,
+               "roofline": {"bound": "hbm", "kernel": "pbfs_kernel", "achieved": per_gpu, "peak": peak,
+                            "unit": "GB/s", "frac": per_gpu / peak, "traffic": None, "peak_source": peak_src,
+                            "bytes_per_launch": sum(byts) / len(byts) / world,
+                            "model": "SURVEY 8(d) algorithmic bytes of the global per-level records / P "
+                                     "(push 12f+4m_f+12d; pull n/4+8u+4e_insp+8d; +8n init)"},
+               "exchange": {"bytes_per_step": sum(xbytes) / len(xbytes),
+                            "bytes_per_level": [l["aux"] for l in lv],
+                            "level_us": [round(l["ns"] / 1e3, 1) for l in lv],
+                            "level_direction": [l["direction"] for l in lv],
+                            "achieved_gbs_per_gpu": nv, "peak_gbs": NVLINK_PEER_GBS,
+                            "frac": nv / NVLINK_PEER_GBS,
+                            "peak_source": "B200_PROFILING.md measured peer copy per direction (900 nominal)"},
+               "gpu_launches": launches, "levels_per_step": statistics.mean(r["num_levels"] for r in recs),
+               "clocks": clk.summary(),
+               "e2e": {"value": sum(edges) / sum(e2e) / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 8 * n,
+                       "what": "collective gr_bfs through the C ABI writing host (pinned) depth+pred of each "
+                               "rank's block; host wall clock, max over ranks"}}
+        if single is not None:
+            out["single_gpu_gteps"] = single
+            out["efficiency"] = {"E": value / (world * single),
+                                 "what": "GTEPS(P) / (P x GTEPS(1)), GTEPS(1) = single-GPU gr_bfs on the "
+                                         "whole graph, same sources, this run"}
+        emit(out)
+    part.close()
+    comm.close()
+    dist.destroy_process_group()
+
+
+def run_partitioned_sssp(args, rank, world, dev):
+    """SSSP over a 1D vertex partition of one graph across all ranks (SURVEY
+    §8(f) f2): strong scaling. Each timed step = one full SSSP; time = max
+    over ranks of the CUDA-event span of the step."""
     import torch
     import torch.distributed as dist
 
@@ -557,17 +724,47 @@ def run_whole_graph(args, rank, world, dev):
         dist.destroy_process_group()
 
 
+def cpu_model():
+    """lscpu model name of this host (the CPU baseline's hardware)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def local_index(dev):
     return dev.index if dev.index is not None else 0
 
 
 # ----------------------------------------------------------------- our arm
 
+def spawn(args):
+    """`bench.py --gpus N` outside torchrun: re-run this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous);
+    rank 0's JSON line goes to this process's stdout."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    r = subprocess.run(cmd, stdout=_JSON_FD, stderr=2)
+    sys.exit(r.returncode)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "--gpus" in " ".join(sys.argv) and args.gpus != world:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -577,13 +774,16 @@ def main():
 
     import graphgen as gg
     import paper_1501_05387_b200 as gr
+    from paper_1501_05387_b200 import metrics
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     dev = torch.device("cuda", local)
     if args.partitioned:
-        return run_partitioned(args, rank, world, dev)
+        if args.prim == "sssp":
+            return run_partitioned_sssp(args, rank, world, dev)
+        return run_partitioned_bfs(args, rank, world, dev)
     if args.prim == "bc":
         return run_bc(args, rank, world, dev)
     if args.prim in ("cc", "pr"):
@@ -612,11 +812,6 @@ def main():
         else:
             G.sssp(s, depth, pred, delta=args.delta, asynchronous=asynchronous)
 
-    def reached(x):
-        if args.prim == "bfs":
-            return int(deg[x >= 0].sum())
-        return int(deg[x != -1].sum())  # uint32 max reads as -1 in int32
-
     for s in warm_srcs:
         step(s)
     torch.cuda.synchronize()
@@ -638,12 +833,13 @@ def main():
         torch.cuda.synchronize()
         timed.launches = gr.gr_kernel_launch_count() - l0
         ms = [a.elapsed_time(b) for a, b in ev]
-        # reached edges and level stats: untimed re-runs (depth is deterministic)
-        edges, recs = 0, []
+        # reached edges (gr_run_stats.reached_edges, A-14) and level stats:
+        # untimed re-runs (depth is deterministic)
+        edges, recs = [], []
         for s in srcs:
             step(s, direction)
-            edges += reached(depth)
             recs.append(G.run_stats())
+            edges.append(recs[-1]["reached_edges"])
         return edges, ms, recs
 
     if world > 1:
@@ -656,6 +852,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     tot_ms = sum(ms)
+    summ = metrics.summarize(edges, ms)
+    edges = sum(edges)
     if world > 1:
         t = torch.tensor([tot_ms, float(edges)], dtype=torch.float64, device=dev)
         tmax = t.clone()
@@ -664,7 +862,7 @@ def main():
         tot_ms_all, edges_all = float(tmax[0]), float(t[1])
     else:
         tot_ms_all, edges_all = tot_ms, float(edges)
-    value = edges_all / (tot_ms_all * 1e-3) / 1e9
+    value = metrics.gteps(edges_all, tot_ms_all * 1e-3)
 
     peak, peak_src = load_peaks()
     byts = [algorithmic_bytes(r, n, args.prim) for r in recs]
@@ -689,7 +887,8 @@ def main():
                       "sources": "%d seeded sources with degree>=1 per rank (S:519)" % args.steps,
                       "l2": "flushed (256 MiB write) between timed steps",
                       "parallelism": "replicas: sources sharded over %d rank(s)" % world},
-           "roofline": roofline, "gpu_launches": launches}
+           "roofline": roofline, "gpu_launches": launches,
+           "throughput": summ if world == 1 else None}
     if rank == 0:
         out["clocks"] = clk.summary()
         out["paper_context"] = PAPER_CONTEXT.get((args.config, args.prim))
@@ -700,7 +899,7 @@ def main():
         pe, pms, precs = timed(my_srcs, "push")
         pb = [algorithmic_bytes(r, n, "bfs") for r in precs]
         pach = sum(pb) / (sum(pms) * 1e-3) / 1e9
-        out["push_only"] = {"value": pe / (sum(pms) * 1e-3) / 1e9, "unit": "GTEPS",
+        out["push_only"] = {"value": metrics.gteps(sum(pe), sum(pms) * 1e-3), "unit": "GTEPS",
                             "ms_per_step": sum(pms) / len(pms), "achieved_gbs": pach,
                             "frac": pach / peak}
         # north-star reading of the bar: "bytes touched per traversed edge x
@@ -728,12 +927,36 @@ def main():
             G.sssp(s, pin_d, pin_p, delta=args.delta)
         per_call.append(time.perf_counter() - t0)
         e2e_s += per_call[-1]
-        e2e_edges += reached(pin_d.to(dev))
+        e2e_edges += G.run_stats()["reached_edges"]
     out["e2e"] = {"value": e2e_edges / e2e_s / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 0,
                   "d2h_bytes_per_step": 8 * n,
                   "what": "gr_bfs/gr_sssp through the C ABI writing host (pinned) depth+pred; "
-                          "host wall clock per call; graph resident (created once, P:1089-1090)",
+                          "host wall clock per call; graph resident (created once, P:1089-1090: the "
+                          "paper's runtimes ignore transfer time); the source id is a call argument",
                   "per_call_ms": [round(x * 1e3, 3) for x in per_call]}
+    if rank == 0 and not args.no_extras:
+        # cold end to end, once (context): gr_graph_create from pinned host CSR
+        # (copy, validation, degree-ordered pull lists, pull head) + one traversal
+        # with host outputs + destroy
+        Rh, Ch = g.R.cpu().pin_memory(), g.C.cpu().pin_memory()
+        Wh = g.W.cpu().pin_memory() if want_w else None
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        Gc = gr.Graph(Rh, Ch, Wh, symmetric=True)
+        t1 = time.perf_counter()
+        if args.prim == "bfs":
+            Gc.bfs(my_srcs[0], pin_d, pin_p, direction=args.direction)
+        else:
+            Gc.sssp(my_srcs[0], pin_d, pin_p, delta=args.delta)
+        t2 = time.perf_counter()
+        ce = Gc.run_stats()["reached_edges"]
+        Gc.close()
+        out["e2e"]["cold"] = {"value": ce / (t2 - t0) / 1e9, "unit": "GTEPS", "create_ms": (t1 - t0) * 1e3,
+                              "traversal_ms": (t2 - t1) * 1e3,
+                              "h2d_bytes": int(Rh.numel() * 8 + Ch.numel() * 4 + (Wh.numel() * 4 if want_w else 0)),
+                              "d2h_bytes": 8 * n,
+                              "what": "one traversal including gr_graph_create from pinned host CSR"}
+        del Rh, Ch, Wh
 
     if rank == 0 and not args.no_cpu_baseline:
         import oracle
@@ -755,7 +978,8 @@ def main():
         out["cpu_baseline"] = {"value": ce / cs / 1e9, "unit": "GTEPS", "cores": 1, "kind": "oracle",
                                "sample": "%d of the timed sources, full %s traversals of %s, "
                                          "single-threaded C oracle (%d host cores available)"
-                                         % (cnt, args.prim, args.config, os.cpu_count())}
+                                         % (cnt, args.prim, args.config, os.cpu_count()),
+                               "cpu_model": cpu_model()}
     if rank == 0:
         emit(out)
     G.close()

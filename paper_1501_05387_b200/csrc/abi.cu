@@ -42,6 +42,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
                   int *launches);
 gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta,
                    int *launches);
+gr_status pbfs_collective(Graph *g, int64_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts &o);
 
 static gr_status finish_run(Graph *g) {
     GR_CUDA(cudaGetLastError());
@@ -116,8 +117,6 @@ gr_status gr_graph_info_get(const gr_graph *h, gr_graph_info *out) {
     out->device = g->device; out->device_bytes = g->bytes;
     return GR_OK;
 }
-
-gr_status pbfs_collective(Graph *g, int64_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts &o);
 
 static gr_status check_bfs_opts(const gr_bfs_opts &o) {
     if (o.direction < 0 || o.direction > 2 || o.strategy < 0 || o.strategy > 2 || o.switch_rule < 0 ||

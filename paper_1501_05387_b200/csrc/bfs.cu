@@ -43,6 +43,7 @@ struct BfsArgs {
     const int32_t *C;
     const int64_t *Rt;   // in-edges for pull (== R when symmetric)
     const int32_t *Ct;
+    const int2 *ph;      // pull head {first in-neighbour, in-degree} per vertex (null: none)
     uint32_t *visited;
     const uint32_t *noin;  // vertices with in-degree 0
     uint32_t *fbuf[3];     // rotating frontier bitmaps
@@ -87,6 +88,7 @@ struct BfsSmemT {
         } small;
     } u;
     unsigned long long ctl[8];
+    unsigned long long wsum[2 * kNW + 2];  // Appender::finish_cta
     long long scan[kNW];
     unsigned long long bsum[6];
     unsigned long long pk[3];   // small mode: packed (edges << kSmallCntBits) | count, per level mod 3
@@ -641,7 +643,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             st.q_valid = 0;
         }
         GR_TSTAMP(5);
-        app.finish();
+        app.finish_cta(s->wsum);
         GR_TSTAMP(6);
         ndisc = warp_sum<unsigned long long>(ndisc);
         insp = warp_sum<unsigned long long>(insp);
@@ -686,7 +688,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
                   int *launches) {
     BfsArgs a;
     a.n = g->n; a.m = g->m;
-    a.R = g->R; a.C = g->C; a.Rt = g->Rt; a.Ct = g->Ct;
+    a.R = g->R; a.C = g->C; a.Rt = g->Rt; a.Ct = g->Ct; a.ph = g->ph;
     a.visited = g->visited;
     a.noin = g->noin;
     for (int i = 0; i < 3; ++i) a.fbuf[i] = g->fbuf[i];

@@ -118,6 +118,7 @@ struct Graph {
     uint32_t *W = nullptr;        // [m] or null
     int64_t *Rt = nullptr;        // CSC (== R when symmetric)
     int32_t *Ct = nullptr;
+    int2 *ph = nullptr;           // pull head: {Ct[Rt[v]] or -1, in-degree} (pull steps, pull.cuh)
 
     // per-run scratch (device)
     uint32_t *visited = nullptr;  // [nwords] visited bitmap (P:793-799 culling)

@@ -28,7 +28,7 @@ void dev_free_all(Graph *g) {
                     g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev,
                     g->sent, g->send_pairs, g->send_counts, g->recv_pairs, g->ps_best, g->ps_sstamp,
                     g->ps_send, g->ps_recv, g->bc_vert, g->bc_sig, g->bc_delta, g->bc_buf, g->bc_cnt,
-                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt};
+                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (g->stats_host) cudaFreeHost(g->stats_host);
@@ -231,6 +231,31 @@ done:
     return st;
 }
 
+// Pull head (pull.cuh): per vertex its first in-list entry -- the highest-
+// degree in-neighbour once lists are ordered -- and its in-degree, so a pull
+// step resolves most candidates with one 8-byte load per vertex instead of
+// a row-offset load followed by a dependent random load into Ct.
+__global__ void pull_head_kernel(const int64_t *Rt, const int32_t *Ct, int64_t n, int2 *ph) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < n; v += nt) {
+        const int64_t b = Rt[v], d = Rt[v + 1] - b;
+        ph[v] = make_int2(d > 0 ? Ct[b] : -1, (int)d);
+    }
+}
+
+gr_status build_pull_head(Graph *g) {
+    if (g->m >= (1ll << 31)) return GR_OK;  // a degree might not fit the int32 field: no head
+    if (!g->ph) {
+        gr_status st = dev_alloc(g, (void **)&g->ph, g->n * sizeof(int2));
+        if (st != GR_OK) return st;
+    }
+    pull_head_kernel<<<g->num_sms * 8, 256, 0, g->stream>>>(g->Rt, g->Ct, g->n, g->ph);
+    count_launch();
+    GR_CUDA(cudaGetLastError());
+    return GR_OK;
+}
+
 static bool is_device_ptr(const void *p) {
     cudaPointerAttributes at;
     if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
@@ -380,6 +405,7 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
         TRY(dev_alloc(g, (void **)&g->qo[i], 2 * n * sizeof(int64_t)));
         TRY(dev_alloc(g, (void **)&g->qr[i], 2 * n * sizeof(int64_t)));
     }
+    if (ncols == n) TRY(build_pull_head(g));  // partitions: after the global list order (pbfs.cu)
     g->pack_shift = bits_for(2 * n + 1);
     TRY(dev_alloc(g, (void **)&g->ctl, sizeof(Ctl)));
     TRYC(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s));

@@ -33,6 +33,7 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
                        uint32_t flags, int device, void *stream, Graph **out, int64_t ncols);
 bool ptr_on_device(const void *p);
 gr_status sort_lists_by_degree(Graph *g, cudaStream_t s, int blocks, const int32_t *deg);
+gr_status build_pull_head(Graph *g);
 
 // ---------------------------------------------------------------- symmetric region
 // Same layout on every rank; peers address it through Graph::sym_peer.
@@ -75,6 +76,7 @@ struct PRank {                 // everything the CTAs of one rank need
     const int64_t *R;
     const int32_t *C;          // push lists (global ids)
     const int32_t *Cp;         // pull lists (global ids, ordered by global neighbour degree)
+    const int2 *ph;            // pull head {first pull-list entry, degree} per owned vertex
     uint32_t *visited;         // local bitmap (authoritative claims of owned vertices)
     const uint32_t *noin;      // local: vertices without in-edges (pre-visited)
     uint32_t *sent;            // global bitmap: remote vertices this rank already shipped
@@ -102,6 +104,7 @@ struct PullView {              // pull_level / bitmap_to_queue view of a partiti
     int64_t n;
     const int64_t *R, *Rt;
     const int32_t *Ct;
+    const int2 *ph;
     uint32_t *visited;
     int32_t *depth, *pred;
 };
@@ -215,6 +218,7 @@ struct PSmem {
         int32_t plist[kNW][kPullList];
     } u;
     PRank r;
+    unsigned long long wsum[2 * kNW + 2];  // Appender::finish_cta
     unsigned long long ctl[16];
     unsigned long long bsum[8];
     int work;
@@ -326,7 +330,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
     app.cap = 2 * a.n_local;
     app.overflow = &a.ctl->overflow;
     const unsigned long long pol_keep = policy_evict_last();
-    const PullView view{a.n_local, a.R, a.R, a.Cp, a.visited, a.depth, a.pred};
+    const PullView view{a.n_local, a.R, a.R, a.Cp, a.ph, a.visited, a.depth, a.pred};
     const uint32_t *gfront_own[2] = {reinterpret_cast<const uint32_t *>(a.sym[a.rank] + A.off_gfront[0]),
                                      reinterpret_cast<const uint32_t *>(a.sym[a.rank] + A.off_gfront[1])};
     const int2 *inbox = reinterpret_cast<const int2 *>(a.sym[a.rank] + A.off_inbox);
@@ -423,7 +427,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
                        (m_u * 4 < M * 3) ? 1 : 0, pol_keep, 0ull, 0ull};
             GlobalFrontier fr{a.qv[L & 1], a.qo[L & 1], a.qr[L & 1], f_loc, mf_loc};
             expand_lb(fr, a.C, gw, nw, op, A.lb_chunks > 0 ? &a.ctl->slot[L & 3].work : nullptr, A.lb_chunks);
-            app.finish();
+            app.finish_cta(sm.wsum);
             ndisc = op.ndisc;
             shipped = op.shipped;
             if (A.nranks > 1) {
@@ -457,7 +461,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
                     }
                     app.push(disc && deg > 0, (int32_t)lw, deg, rs);
                 }
-                app.finish();
+                app.finish_cta(sm.wsum);
                 istart = iend;
             }
             fb_valid = fbn_clean;
@@ -544,7 +548,7 @@ static void fill_rank(Graph *g, PRank &r, int32_t *depth, int32_t *pred) {
     r.rank = g->comm->rank;
     r.S = g->pack_shift;
     r.n_local = g->n; r.v_begin = g->v_begin; r.m_local = g->m; r.nonisolated = g->nonisolated;
-    r.R = g->R; r.C = g->C; r.Cp = g->Ct;
+    r.R = g->R; r.C = g->C; r.Cp = g->Ct; r.ph = g->ph;
     r.visited = g->visited; r.noin = g->noin; r.sent = g->sent;
     for (int i = 0; i < 3; ++i) r.fb[i] = g->fbuf[i];
     for (int i = 0; i < 2; ++i) { r.qv[i] = g->qv[i]; r.qo[i] = g->qo[i]; r.qr[i] = g->qr[i]; }
@@ -589,6 +593,7 @@ static gr_status prepare_real(Graph *g) {
     count_launch();
     gr_status st = comm_allgather_bytes(c, deg, deg + g->block, per, g->stream);
     if (st == GR_OK && !(g->flags_keep_order)) st = order_pull_lists(&g, 1, deg + g->block);
+    if (st == GR_OK) st = build_pull_head(g);
     cudaStreamSynchronize(g->stream);
     cudaFree(deg);
     if (st == GR_OK) g->prepared = true;
@@ -610,6 +615,7 @@ static gr_status prepare_loopback(LoopGroup *grp) {
     GR_CUDA(cudaStreamSynchronize(g0->stream));
     gr_status st = GR_OK;
     if (!g0->flags_keep_order) st = order_pull_lists(grp->graphs, P, deg);
+    for (int r = 0; r < P && st == GR_OK; ++r) st = build_pull_head(grp->graphs[r]);
     cudaDeviceSynchronize();
     cudaFree(deg);
     if (st == GR_OK)

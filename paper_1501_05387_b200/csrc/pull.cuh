@@ -44,7 +44,7 @@ struct PullCounts {
     unsigned dmax = 0;
 };
 
-// A: any view with n, R, Rt, Ct, visited, depth, pred (BfsArgs; the
+// A: any view with n, R, Rt, Ct, ph, visited, depth, pred (BfsArgs; the
 // partitioned kernel's PullView, whose in-lists hold GLOBAL ids probed in the
 // all-gathered frontier `fcur` while x, visited, depth, pred and fnext are
 // local). [wb0, wb1): this CTA's range of visited-bitmap words.
@@ -69,18 +69,40 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
         bool fnd[2];
 #pragma unroll
         for (int q = 0; q < 2; ++q) v[q] = ((int)l + 32 * q < k) ? wl[l + 32 * q] : -1;
+        if (a.ph) {
+            // pull head {first in-neighbour, in-degree}: one 8-byte load per
+            // candidate (consecutive candidates -> coalesced) answers most of
+            // them (in-lists are ordered by neighbour degree, hubs first);
+            // only unresolved lists read their row offset
+            int2 h[2];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            beg[q] = v[q] >= 0 ? a.Rt[v[q]] : 0;
-            end[q] = v[q] >= 0 ? a.Rt[v[q] + 1] : 0;
-        }
+            for (int q = 0; q < 2; ++q) h[q] = v[q] >= 0 ? __ldg(a.ph + v[q]) : make_int2(-1, 0);
 #pragma unroll
-        for (int q = 0; q < 2; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Ct + beg[q], pol) : -1;
+            for (int q = 0; q < 2; ++q) {
+                u0[q] = h[q].x;
+                fnd[q] = u0[q] >= 0 && fbit(u0[q]);
+                par[q] = u0[q];
+                pc.insp += (u0[q] >= 0);
+            }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-            fnd[q] = u0[q] >= 0 && fbit(u0[q]);
-            par[q] = u0[q];
-            pc.insp += (u0[q] >= 0);
+            for (int q = 0; q < 2; ++q) {
+                beg[q] = (!fnd[q] && h[q].y > 1) ? a.Rt[v[q]] : 0;
+                end[q] = beg[q] + h[q].y;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                beg[q] = v[q] >= 0 ? a.Rt[v[q]] : 0;
+                end[q] = v[q] >= 0 ? a.Rt[v[q] + 1] : 0;
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Ct + beg[q], pol) : -1;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                fnd[q] = u0[q] >= 0 && fbit(u0[q]);
+                par[q] = u0[q];
+                pc.insp += (u0[q] >= 0);
+            }
         }
         // the rest of each unresolved list: first by its lane (4 edges a step,
         // at most kPullLong edges), then what is left of the long ones by the

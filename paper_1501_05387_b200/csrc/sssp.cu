@@ -55,6 +55,7 @@ struct SsspSmem {
     int32_t fv[kWarpsPerBlock][kSsspStage];   // far staging
     unsigned long long ctl[8];
     unsigned long long bsum[4];
+    unsigned long long wsum[2 * kWarpsPerBlock + 2];  // Appender::finish_cta
     int win;  // expand_twc: CTA arbitration
 };
 
@@ -232,8 +233,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
 #else
                 expand_lb(fr, a.C, gw, nw, op, &a.ctl->slot[k & 3].work, 4);
 #endif
-            nearq.finish();
-            farq.finish();
+            nearq.finish_cta(s->wsum);
+            farq.finish_cta(s->wsum);
             const unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
             if (lane_id() == 0 && ni) atomicAdd(&s->bsum[0], ni);
             __syncthreads();
@@ -294,8 +295,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
                 nearq.push(to_near && deg > 0, v, deg, rs);
                 farq.push(to_far, v, 0);
             }
-            nearq.finish();
-            farq.finish();
+            nearq.finish_cta(s->wsum);
+            farq.finish_cta(s->wsum);
             grid.sync();
             fp ^= 1;
         }

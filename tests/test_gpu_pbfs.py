@@ -93,9 +93,9 @@ def test_loopback_rules_and_keep_order(mg):
 def test_loopback_isolated_source_and_tiny(mg):
     """An isolated source (one level), a 2-vertex graph over 2 ranks, a path
     crossing every rank boundary (one remote ship per level)."""
-    g = gg.from_edges(70, [(i, i + 1) for i in range(60)] + [(65, 66)])
+    g = gg.from_edges(200, [(i, i + 1) for i in range(190)] + [(195, 196)])  # blocks of 64
     comms, parts = _loopback_graphs(mg, g, 4)
-    _run_check(parts, g, [0, 30, 62, 69, 65], directions=("auto", "push", "pull"))
+    _run_check(parts, g, [0, 100, 190, 199, 195], directions=("auto", "push", "pull"))
     _close(comms, parts)
     g = gg.from_edges(2, [(0, 1)])
     comms, parts = _loopback_graphs(mg, g, 1)
