@@ -643,8 +643,6 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             st.q_valid = 0;
         }
         GR_TSTAMP(5);
-        app.finish_cta(s->wsum);
-        GR_TSTAMP(6);
         ndisc = warp_sum<unsigned long long>(ndisc);
         insp = warp_sum<unsigned long long>(insp);
         if (lane_id() == 0) {
@@ -656,7 +654,8 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             atomicMax(&s->bsum[3], tw);
 #endif
         }
-        __syncthreads();
+        app.finish_cta(s->wsum);  // its CTA barriers also complete the counters above
+        GR_TSTAMP(6);
 #ifdef GR_TRACE
         if (g_bal && threadIdx.x == 0 && L < 64) {
             g_bal[((int64_t)L * gridDim.x + blockIdx.x) * 2] = (long long)s->bsum[2];

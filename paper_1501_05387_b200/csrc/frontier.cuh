@@ -330,17 +330,22 @@ __device__ __forceinline__ int64_t warp_lower_bound(int64_t F, int64_t t, Key ke
 //                   contiguous in edge space, so deg(j) = qo[j+1] - qo[j].
 //   SmemFrontier:   the same three arrays in shared memory (single-CTA levels).
 // ---------------------------------------------------------------------------
+// The queue of a level was written by the previous level (before a grid
+// barrier, whose fence makes it visible): plain loads, cached in L1, so the
+// warps of an SM share one L2 request per line -- with a small frontier every
+// warp of the grid searches and loads the SAME few lines (an L2 hot spot
+// with L2-only loads).
 struct GlobalFrontier {
     const int32_t *qv;
     const int64_t *qo;
     const int64_t *qr;
     int64_t F, E;
-    __device__ __forceinline__ int64_t off(int64_t i) const { return __ldcg(qo + i); }
+    __device__ __forceinline__ int64_t off(int64_t i) const { return qo[i]; }
     __device__ __forceinline__ void load(int64_t j, int32_t &v, int64_t &o, int64_t &rs, int64_t &end) const {
-        v = __ldcg(qv + j);
-        o = __ldcg(qo + j);
-        rs = __ldcg(qr + j);
-        end = (j + 1 < F) ? __ldcg(qo + j + 1) : E;
+        v = qv[j];
+        o = qo[j];
+        rs = qr[j];
+        end = (j + 1 < F) ? qo[j + 1] : E;
     }
 };
 

@@ -25,6 +25,7 @@
 // ranks in one process on one GPU) runs every rank in ONE cooperative launch,
 // CTA block [r*ctas, (r+1)*ctas) acting as rank r: the multi-rank logic is the
 // same code, tested on one GPU.
+#include "part.cuh"
 #include "pull.cuh"
 
 namespace gr {
@@ -34,40 +35,6 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
 bool ptr_on_device(const void *p);
 gr_status sort_lists_by_degree(Graph *g, cudaStream_t s, int blocks, const int32_t *deg);
 gr_status build_pull_head(Graph *g);
-
-// ---------------------------------------------------------------- symmetric region
-// Same layout on every rank; peers address it through Graph::sym_peer.
-struct SymHdr {
-    unsigned long long flag[kMaxRanks];       // barrier: flag[q] = epoch of rank q's last arrival here
-    unsigned long long inbox_count;           // (vertex, parent) pairs stored into this rank's inbox this run
-    unsigned long long pad0[7];
-    unsigned long long st[2][kMaxRanks][8];   // per level parity, per sender rank: published counters
-};
-// st fields (the next local frontier of the sender, after its level):
-enum { kStF = 0, kStMf = 1, kStDisc = 2, kStOvf = 3, kStInsp = 4, kStShip = 5, kStDmax = 6, kStAux = 7 };
-// level-0 table: kStInsp = m_local, kStAux = non-isolated local vertices
-constexpr size_t kSymHdrBytes = 4096;
-static_assert(sizeof(SymHdr) <= kSymHdrBytes, "symmetric header");
-
-struct SymLayout {
-    size_t gfront[2];    // global frontier bitmaps (all-gathered shards), by pull-level parity
-    size_t inbox;        // int2 (vertex, parent) pairs shipped to this rank
-    int64_t inbox_cap;   // pairs: (P-1) * block (each peer ships a vertex at most once per run)
-    int64_t gwords;      // words of a global bitmap (P * block / 32)
-    size_t bytes;
-};
-
-static SymLayout sym_layout(int P, int64_t block) {
-    SymLayout L;
-    L.gwords = (int64_t)P * block / 32;
-    const size_t gb = ((size_t)L.gwords * 4 + 255) & ~(size_t)255;
-    L.gfront[0] = kSymHdrBytes;
-    L.gfront[1] = L.gfront[0] + gb;
-    L.inbox = L.gfront[1] + gb;
-    L.inbox_cap = P > 1 ? (int64_t)(P - 1) * block : 1;
-    L.bytes = L.inbox + (size_t)L.inbox_cap * 8;
-    return L;
-}
 
 // ---------------------------------------------------------------- kernel arguments
 struct PRank {                 // everything the CTAs of one rank need
@@ -108,20 +75,6 @@ struct PullView {              // pull_level / bitmap_to_queue view of a partiti
     uint32_t *visited;
     int32_t *depth, *pred;
 };
-
-__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ long long pgtimer() {
-    long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 
 // ---------------------------------------------------------------------------
 // Fused cond/apply + filter + exchange of a push level (per edge (s, w)):
@@ -245,42 +198,10 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
     const int64_t gwords = (A.n_global + 31) / 32;              // global bitmap words
     const unsigned long long cmask = (1ull << a.S) - 1;
     const bool lead = bid == 0 && threadIdx.x == 0;             // one thread per rank
-    auto hdr = [&](int q) { return reinterpret_cast<SymHdr *>(a.sym[q]); };
-    unsigned long long ep = a.ctl->epoch;                       // barrier epochs so far (multi-process)
-
-    // cross-process half of a barrier, between two grid barriers: thread q of
-    // the rank's first CTA announces this rank's arrival to rank q and waits
-    // for rank q's (a dead peer ends the wait after 20 s with overflow = 3)
-    auto peer_flags = [&]() {
-        ++ep;
-        if (bid == 0 && (int)threadIdx.x < A.nranks) {
-            const int q = threadIdx.x;
-            __threadfence_system();
-            st_release_sys(&hdr(q)->flag[a.rank], ep);
-            const long long t0 = pgtimer();
-            while (ld_acquire_sys(&hdr(a.rank)->flag[q]) < ep) {
-                if (pgtimer() - t0 > 20000000000ll) { atomicExch(&a.ctl->overflow, 3ull); break; }
-            }
-        }
-    };
-    auto gbar = [&]() {  // barrier of every rank of the group
-        grid.sync();
-        if (A.multiproc) {
-            peer_flags();
-            grid.sync();
-        }
-    };
-    // publishes this rank's counters into every rank's table (par), then barrier
-    auto publish = [&](int par, const unsigned long long *vals) {
-        if (lead)
-            for (int q = 0; q < A.nranks; ++q)
-                for (int k = 0; k < 8; ++k) hdr(q)->st[par][a.rank][k] = vals[k];
-        if (A.multiproc) {
-            __syncthreads();
-            peer_flags();
-        }
-        grid.sync();
-    };
+    RankSync rs{&grid, a.sym, a.rank, A.nranks, A.multiproc, bid, a.ctl, a.ctl->epoch};
+    auto hdr = [&](int q) { return rs.hdr(q); };
+    auto gbar = [&]() { rs.bar(); };
+    auto publish = [&](int par, const unsigned long long *vals) { rs.publish(par, vals); };
 
     // ---- Set_Problem_Data on the owned block ------------------
     for (int64_t v = tid; v < a.n_local; v += nthreads) {
@@ -344,16 +265,8 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
     for (;;) {
         const int par = L & 1;
         if (threadIdx.x == 0) {
-            unsigned long long t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int q = 0; q < A.nranks; ++q) {
-                const unsigned long long *row = hdr(a.rank)->st[par][q];
-                for (int k = 0; k < 8; ++k) {
-                    const unsigned long long x = __ldcg(row + k);
-                    if (k == kStOvf) t[k] |= x;
-                    else if (k == kStDmax) t[k] = max(t[k], x);
-                    else t[k] += x;
-                }
-            }
+            unsigned long long t[8];
+            rs.read(par, t, kStDmax, kStOvf);
             for (int k = 0; k < 8; ++k) sm.ctl[k] = t[k];
             sm.ctl[8] = ld_relaxed(&a.ctl->slot[L & 3].qpack);
             sm.work = 0;
@@ -395,8 +308,8 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
             sr.ns = 0;
         }
         if (tid == 0) {
-            Slot &rs = a.ctl->slot[(L + 2) & 3];
-            rs.qpack = 0; rs.ndisc = 0; rs.fpack = 0; rs.work = 0; rs.insp = 0; rs.dmax = 0; rs.pad[0] = 0;
+            Slot &rst = a.ctl->slot[(L + 2) & 3];
+            rst.qpack = 0; rst.ndisc = 0; rst.fpack = 0; rst.work = 0; rst.insp = 0; rst.dmax = 0; rst.pad[0] = 0;
         }
         Slot &nxt = a.ctl->slot[(L + 1) & 3];
         app.qv = a.qv[(L + 1) & 1];
@@ -537,7 +450,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
     }
     if (lead) {
         a.ctl->levels = (unsigned long long)L;
-        a.ctl->epoch = ep;
+        a.ctl->epoch = rs.ep;
         if (a.ctl->overflow) a.ctl->sticky = 1ull;
     }
 }
@@ -628,7 +541,7 @@ static gr_status prepare_loopback(LoopGroup *grp) {
 static gr_status launch_pbfs(Graph **gs, int k, int64_t src, int32_t **depth, int32_t **pred, const gr_bfs_opts &o) {
     Graph *g0 = gs[0];
     Comm *c = g0->comm;
-    const SymLayout Ly = sym_layout(c->nranks, g0->block);
+    const SymLayout Ly = sym_layout(c->nranks, g0->block, g0->has_w && g0->W);
     PBfsArgs A;
     memset(&A, 0, sizeof(A));
     for (int i = 0; i < k; ++i) fill_rank(gs[i], A.ranks[i], depth[i], pred[i]);
@@ -795,7 +708,7 @@ gr_status gr_graph_create_partitioned(gr_comm *ch, int64_t n_global, int64_t v_b
     g->nparts = P; g->rank = c->rank;
     g->has_w = weights != nullptr || m_local == 0;
     g->flags_keep_order = (flags & GR_KEEP_ORDER) != 0;
-    const SymLayout Ly = sym_layout(P, block);
+    const SymLayout Ly = sym_layout(P, block, weights != nullptr && m_local > 0);
     if ((st = dev_alloc(g, (void **)&g->sent, ((n_global + 31) / 32) * sizeof(uint32_t))) != GR_OK ||
         (st = comm_sym_alloc(c, g, Ly.bytes)) != GR_OK) {
         comm_sym_free(g);

@@ -19,7 +19,7 @@ G.bfs(s)
 torch.cuda.synchronize()
 t = tr.view(256, 16).cpu().numpy()
 st = G.run_stats()["levels"]
-for L in list(range(0, 12)) + list(range(100, 106)):
+for L in [x for x in list(range(0, 12)) + list(range(100, 106)) if x + 1 < len(st)]:
     row = t[L]
     base = row[0]
     if base == 0:
