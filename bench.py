@@ -262,17 +262,18 @@ def partitioned_bytes(levels, n, nonisolated):
     return B
 
 
-def run_partitioned_bfs(args, rank, world, dev):
-    """BASELINE config 5: BFS over a 1D vertex partition of one graph across
-    all ranks through the library's own group
-    (gr_comm_create: NCCL communicator bootstrapped from a torch.distributed
-    broadcast of the unique id) and collective gr_bfs on
-    gr_graph_create_partitioned graphs: one persistent kernel per rank runs
-    every level, exchange included (peer-memory stores over NVLink). Strong
-    scaling: the graph is fixed, each rank owns n/P vertices. Each timed step
-    = one full BFS; time = max over ranks of the CUDA-event span of the call.
-    E(P) = GTEPS(P) / (P * GTEPS(1)), GTEPS(1) = rank 0's single-GPU kernel
-    (gr_bfs on the whole graph) on the same sources, measured in this run."""
+def run_partitioned(args, rank, world, dev):
+    """BASELINE config 5: BFS (or, --prim sssp, delta-stepping SSSP: SURVEY
+    §8(f) f2) over a 1D vertex partition of one graph across all ranks
+     through the library's own group (gr_comm_create:
+    NCCL communicator bootstrapped from a torch.distributed broadcast of the
+    unique id) and collective gr_bfs / gr_sssp on gr_graph_create_partitioned
+    graphs: one persistent kernel per rank runs every level, exchange
+    included (peer-memory stores over NVLink). Strong scaling: the graph is
+    fixed, each rank owns n/P vertices. Each timed step = one full traversal;
+    time = max over ranks of the CUDA-event span of the call. E(P) =
+    GTEPS(P) / (P * GTEPS(1)), GTEPS(1) = rank 0's single-GPU kernel (gr_bfs /
+    gr_sssp on the whole graph) on the same sources, measured in this run."""
     import torch
     import torch.distributed as dist
 
@@ -284,7 +285,8 @@ def run_partitioned_bfs(args, rank, world, dev):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29517")
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
-    g = gg.make_config(args.config, device=dev)
+    sssp = args.prim == "sssp"
+    g = gg.make_config(args.config, device=dev, weights=True if sssp else None)
     n, m = g.n, g.m
     srcs = gg.sources(g, args.warmup + args.steps)
     nonisolated = int((g.R[1:] > g.R[:-1]).sum())
@@ -292,16 +294,22 @@ def run_partitioned_bfs(args, rank, world, dev):
     # single-GPU reference for E(P): rank 0, whole graph, same sources
     single = None
     if rank == 0 and not args.no_extras:
-        G = gr.Graph(g.R, g.C, None, symmetric=True)
+        G = gr.Graph(g.R, g.C, g.W if sssp else None, symmetric=True)
         d1 = torch.empty(n, dtype=torch.int32, device=dev)
+
+        def one(s):
+            if sssp:
+                G.sssp(s, d1, None, delta=args.delta)
+            else:
+                G.bfs(s, d1, None)
         for s in srcs[: args.warmup]:
-            G.bfs(s, d1, None)
+            one(s)
         e1s, ms1 = 0, 0.0
         for s in srcs[args.warmup:]:
             flush.zero_()
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a0.record()
-            G.bfs(s, d1, None)
+            one(s)
             a1.record()
             torch.cuda.synchronize()
             ms1 += a0.elapsed_time(a1)
@@ -309,17 +317,22 @@ def run_partitioned_bfs(args, rank, world, dev):
         single = metrics.gteps(e1s, ms1 * 1e-3)
         G.close()
         del d1
-    v0, v1, Rl, Cl, _ = mg.partition_csr(g.R, g.C, world, rank)
+    v0, v1, Rl, Cl, Wl = mg.partition_csr(g.R, g.C, world, rank, W=g.W if sssp else None)
     del g
     torch.cuda.empty_cache()
     comm = mg.Comm.from_torch(dev.index)
-    part = mg.PartitionedGraph(comm, Rl, Cl, n)
-    del Rl, Cl
+    part = mg.PartitionedGraph(comm, Rl, Cl, n, W_local=Wl)
+    del Rl, Cl, Wl
+
+    def run(s, d, p):
+        if sssp:
+            return part.sssp(s, d, p, delta=args.delta)
+        return part.bfs(s, d, p)
     torch.cuda.empty_cache()
     depth = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
     pred = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
     for s in srcs[: args.warmup]:
-        part.bfs(s, depth, pred)
+        run(s, depth, pred)
     dist.barrier()
     torch.cuda.synchronize()
     launches0 = gr.gr_kernel_launch_count()
@@ -330,7 +343,7 @@ def run_partitioned_bfs(args, rank, world, dev):
             dist.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            part.bfs(s, depth, pred)
+            run(s, depth, pred)
             e1.record()
             torch.cuda.synchronize()
             st = part.run_stats()
@@ -345,12 +358,12 @@ def run_partitioned_bfs(args, rank, world, dev):
     # end to end through the C ABI: host (pinned) outputs, host wall clock, max over ranks
     pin_d = torch.empty(v1 - v0, dtype=torch.int32, pin_memory=True)
     pin_p = torch.empty(v1 - v0, dtype=torch.int32, pin_memory=True)
-    part.bfs(srcs[0], pin_d, pin_p)
+    run(srcs[0], pin_d, pin_p)
     e2e = []
     for s in srcs[args.warmup:]:
         dist.barrier()
         t0 = time.perf_counter()
-        part.bfs(s, pin_d, pin_p)
+        run(s, pin_d, pin_p)
         t = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e.append(float(t[0]))
@@ -359,7 +372,8 @@ def run_partitioned_bfs(args, rank, world, dev):
         summ = metrics.summarize(edges, ms)
         value = summ["aggregate"]
         peak, peak_src = load_peaks()
-        byts = [partitioned_bytes(r["levels"], n, nonisolated) for r in recs]
+        byts = [algorithmic_bytes(r, n, "sssp") if sssp else partitioned_bytes(r["levels"], n, nonisolated)
+                for r in recs]
         xbytes = [sum(l["aux"] for l in r["levels"]) for r in recs]
         tot_s = sum(ms) * 1e-3
         per_gpu = sum(byts) / world / tot_s / 1e9
@@ -367,20 +381,26 @@ def run_partitioned_bfs(args, rank, world, dev):
         lv = recs[-1]["levels"]
         out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": sum(ms) / len(ms), "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-               "config": {"workload": "%s bfs 1D-partitioned direction-optimizing, fused exchange over peer "
-                                      "memory (gr_comm + gr_graph_create_partitioned + collective gr_bfs)"
-                                      % args.config,
+               "scaling": "strong", "vs_baseline": None, "dtype": "u32" if sssp else "int32",
+               "data": "synthetic",
+               "config": {"workload": ("%s sssp 1D-partitioned near/far delta-stepping (delta %d), fused exchange "
+                                       "over peer memory (gr_comm + gr_graph_create_partitioned + collective "
+                                       "gr_sssp)" % (args.config, recs[-1]["delta"])) if sssp else
+                                      ("%s bfs 1D-partitioned direction-optimizing, fused exchange over peer "
+                                       "memory (gr_comm + gr_graph_create_partitioned + collective gr_bfs)"
+                                       % args.config),
                           "graph": CONFIG_DESC[args.config], "n": n, "m": m,
                           "sources": "%d seeded sources with degree>=1 (S:519)" % args.steps,
                           "parallelism": "1D vertex partition over %d rank(s), one persistent kernel per rank" % world,
                           "l2": "flushed (256 MiB write) between timed steps"},
                "throughput": summ,
-               "roofline": {"bound": "hbm", "kernel": "pbfs_kernel", "achieved": per_gpu, "peak": peak,
+               "roofline": {"bound": "hbm", "kernel": "psssp_kernel" if sssp else "pbfs_kernel",
+                            "achieved": per_gpu, "peak": peak,
                             "unit": "GB/s", "frac": per_gpu / peak, "traffic": None, "peak_source": peak_src,
                             "bytes_per_launch": sum(byts) / len(byts) / world,
                             "model": "SURVEY 8(d) algorithmic bytes of the global per-level records / P "
-                                     "(push 12f+4m_f+12d; pull n/4+8u+4e_insp+8d; +8n init)"},
+                                     + ("(relax 16f+8e+12r; re-split 8|far|; +12n init)" if sssp else
+                                        "(push 12f+4m_f+12d; pull n/4+8u+4e_insp+8d; +8n init)")},
                "exchange": {"bytes_per_step": sum(xbytes) / len(xbytes),
                             "bytes_per_level": [l["aux"] for l in lv],
                             "level_us": [round(l["ns"] / 1e3, 1) for l in lv],
@@ -402,96 +422,6 @@ def run_partitioned_bfs(args, rank, world, dev):
         emit(out)
     part.close()
     comm.close()
-    dist.destroy_process_group()
-
-
-def run_partitioned_sssp(args, rank, world, dev):
-    """SSSP over a 1D vertex partition of one graph across all ranks (SURVEY
-    §8(f) f2): strong scaling. Each timed step = one full SSSP; time = max
-    over ranks of the CUDA-event span of the step."""
-    import torch
-    import torch.distributed as dist
-
-    import graphgen as gg
-    import paper_1501_05387_b200 as gr
-    from paper_1501_05387_b200 import dist as grd
-    if world == 1 and not dist.is_initialized():
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("MASTER_PORT", "29517")
-        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
-    sssp = args.prim == "sssp"
-    g = gg.make_config(args.config, device=dev, weights=True if sssp else None)
-    srcs = gg.sources(g, args.warmup + args.steps)
-    v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, world, rank)
-    Wl = grd.partition_weights(g.R, g.W, world, rank) if sssp else None
-    deg_local = (Rl[1:] - Rl[:-1])
-    n, m = g.n, g.m
-    delta = args.delta
-    if sssp and delta == 0:  # the single-GPU auto rule (reading A-10, abi.cu)
-        mw = int(g.W.max())
-        delta = max(1, (mw + 10) // 21) if m / n >= 8.0 else mw * 32
-    part = grd.GpuPartition(Rl, Cl, n, world, rank, device=dev.index, W_local=Wl)
-    del g
-    torch.cuda.empty_cache()
-    ex = grd.TorchDistExchange()
-    if not sssp and not args.keep_order:  # pull lists by global neighbour degree (a7; as on one GPU)
-        part.order_pull_lists(grd.global_degrees(part, ex))
-    depth = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
-    pred = torch.empty(v1 - v0, dtype=torch.int32, device=dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
-
-    def run(s):
-        if sssp:
-            return grd.sssp_partitioned(part, ex, s, depth, pred, delta=delta)
-        return grd.bfs_partitioned(part, ex, s, depth, pred)
-
-    for s in srcs[: args.warmup]:
-        run(s)
-    dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = gr.gr_kernel_launch_count()
-    tot_ms, edges, levels = 0.0, 0, []
-    with Clocks(dev.index) as clk:
-        for s in srcs[args.warmup:]:
-            flush.zero_()
-            dist.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
-            levels.append(run(s))
-            e1.record()
-            torch.cuda.synchronize()
-            t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            tot_ms += float(t[0])
-            reached = (depth != -1) if sssp else (depth >= 0)  # uint32 max reads as -1
-            r = torch.tensor([int(deg_local[reached].sum())], dtype=torch.int64, device=dev)
-            dist.all_reduce(r)
-            edges += int(r[0])
-    launches = gr.gr_kernel_launch_count() - launches0
-    dist.barrier()
-    value = edges / (tot_ms * 1e-3) / 1e9
-    if rank == 0:
-        out = {"metric": METRIC, "value": value, "unit": "GTEPS", "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "u32" if sssp else "int32",
-               "data": "synthetic",
-               "config": {"workload": ("%s sssp 1D-partitioned near/far delta-stepping (delta %d): NCCL "
-                                       "all-to-all of (vertex,dist,parent) triples per near iteration, "
-                                       "all-reduced far minimum per re-split" % (args.config, delta)) if sssp else
-                                      ("%s bfs 1D-partitioned direction-optimizing: push levels "
-                                       "NCCL all-to-all of (vertex,parent), pull levels NCCL all-gather "
-                                       "of the frontier bitmap" % args.config),
-                          "graph": CONFIG_DESC[args.config], "n": n, "m": m,
-                          "parallelism": "1D vertex partition over %d rank(s)" % world,
-                          "pull_lists": "caller order" if (sssp or args.keep_order)
-                          else "ordered by global neighbour degree (gr_part_order_pull_lists)",
-                          "l2": "flushed (256 MiB write) between timed steps"},
-               "gpu_launches": launches, "levels_per_step": sum(levels) / len(levels),
-               "clocks": clk.summary(),
-               "roofline": None,
-               "e2e": None}
-        emit(out)
-    part.close()
     dist.destroy_process_group()
 
 
@@ -781,9 +711,7 @@ def main():
 
     dev = torch.device("cuda", local)
     if args.partitioned:
-        if args.prim == "sssp":
-            return run_partitioned_sssp(args, rank, world, dev)
-        return run_partitioned_bfs(args, rank, world, dev)
+        return run_partitioned(args, rank, world, dev)
     if args.prim == "bc":
         return run_bc(args, rank, world, dev)
     if args.prim in ("cc", "pr"):

@@ -43,6 +43,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
 gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta,
                    int *launches);
 gr_status pbfs_collective(Graph *g, int64_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts &o);
+gr_status psssp_collective(Graph *g, int64_t src, uint32_t *dist_out, int32_t *pred_out, uint32_t delta);
 
 static gr_status finish_run(Graph *g) {
     GR_CUDA(cudaGetLastError());
@@ -286,6 +287,17 @@ static gr_status sssp_args(gr_graph *h, int32_t src, const uint32_t *dist_out, c
 
 gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_out, const gr_sssp_opts *opts) {
     g_err[0] = 0;
+    if (h && ((Graph *)h)->comm) {  // partitioned graph: collective over the comm's ranks (psssp.cu)
+        Graph *g = (Graph *)h;
+        if (!dist_out) { set_error("dist_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
+        if (src < 0 || src >= g->n_global) {
+            set_error("src=%d not in [0, n=%lld)", src, (long long)g->n_global);
+            return GR_ERR_OUT_OF_RANGE;
+        }
+        gr_sssp_opts o = opts ? *opts : gr_sssp_opts{};
+        if (o.strategy < 0 || o.strategy > 2) { set_error("invalid gr_sssp_opts"); return GR_ERR_INVALID_ARGUMENT; }
+        return psssp_collective(g, src, dist_out, pred_out, o.delta);
+    }
     uint64_t delta = 0;
     gr_status st = sssp_args(h, src, dist_out, opts, &delta);
     if (st != GR_OK) return st;
@@ -318,6 +330,10 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
 gr_status gr_sssp_async(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_out,
                         const gr_sssp_opts *opts) {
     g_err[0] = 0;
+    if (h && ((Graph *)h)->comm) {
+        set_error("gr_sssp_async: a partitioned graph runs collective synchronous gr_sssp calls");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
     uint64_t delta = 0;
     gr_status st = sssp_args(h, src, dist_out, opts, &delta);
     if (st != GR_OK) return st;

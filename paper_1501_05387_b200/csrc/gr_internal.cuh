@@ -64,7 +64,7 @@ struct Ctl {
     Slot slot[kSlots];
     unsigned long long overflow;   // set when a queue capacity would be exceeded
     unsigned long long levels;     // levels executed by the last run
-    unsigned long long reached;    // (unused by kernels; host bookkeeping)
+    unsigned long long reached;    // psssp.cu: length of the current step's ship list
     unsigned long long far_count[2];
     long long bstate[8];           // small-mode handoff of the traversal state
     unsigned long long sticky;     // some run since the last gr_graph_sync overflowed
@@ -178,6 +178,8 @@ struct Graph {
     bool flags_keep_order = false;     // GR_KEEP_ORDER: keep the caller's pull-list order
     void *pbfs_ranks = nullptr;        // device table of the ranks a launch hosts (pbfs.cu PRank)
     int64_t m_global = 0, nonisolated_global = 0;
+    uint32_t maxw_global = 0;
+    int32_t *ps_ship = nullptr;             // [n_global] vertices shipped in the current step (psssp.cu)
     // partitioned SSSP (partition_sssp.cu)
     unsigned long long *ps_best = nullptr;  // [n_global] best (dist<<32|pred) shipped per remote vertex
     int32_t *ps_sstamp = nullptr;           // [n_global] step of the last shipment (one per step)

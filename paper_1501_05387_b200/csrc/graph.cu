@@ -28,7 +28,7 @@ void dev_free_all(Graph *g) {
                     g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev,
                     g->sent, g->send_pairs, g->send_counts, g->recv_pairs, g->ps_best, g->ps_sstamp,
                     g->ps_send, g->ps_recv, g->bc_vert, g->bc_sig, g->bc_delta, g->bc_buf, g->bc_cnt,
-                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph};
+                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph, g->ps_ship};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (g->stats_host) cudaFreeHost(g->stats_host);

@@ -497,7 +497,7 @@ static gr_status order_pull_lists(Graph **gs, int k, const int32_t *deg_global) 
     return GR_OK;
 }
 
-static gr_status prepare_real(Graph *g) {
+gr_status prepare_real(Graph *g) {
     Comm *c = g->comm;
     int32_t *deg = nullptr;
     const size_t per = (size_t)g->block * sizeof(int32_t);
@@ -505,6 +505,22 @@ static gr_status prepare_real(Graph *g) {
     pdeg_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->R, g->n, g->block, deg);
     count_launch();
     gr_status st = comm_allgather_bytes(c, deg, deg + g->block, per, g->stream);
+    if (st == GR_OK) {  // global totals: m, max weight, non-isolated vertices
+        long long mine[3] = {(long long)g->m, (long long)g->max_w, (long long)g->nonisolated};
+        long long *d3 = nullptr;
+        GR_CUDA(cudaMalloc((void **)&d3, sizeof(mine) * (c->nranks + 1)));
+        GR_CUDA(cudaMemcpy(d3, mine, sizeof(mine), cudaMemcpyHostToDevice));
+        st = comm_allgather_bytes(c, d3, d3 + 3, sizeof(mine), g->stream);
+        long long all[3 * kMaxRanks];
+        if (st == GR_OK) GR_CUDA(cudaMemcpy(all, d3 + 3, sizeof(mine) * c->nranks, cudaMemcpyDeviceToHost));
+        cudaFree(d3);
+        g->m_global = 0; g->maxw_global = 0; g->nonisolated_global = 0;
+        for (int q = 0; q < c->nranks && st == GR_OK; ++q) {
+            g->m_global += all[3 * q];
+            g->maxw_global = all[3 * q + 1] > (long long)g->maxw_global ? (uint32_t)all[3 * q + 1] : g->maxw_global;
+            g->nonisolated_global += all[3 * q + 2];
+        }
+    }
     if (st == GR_OK && !(g->flags_keep_order)) st = order_pull_lists(&g, 1, deg + g->block);
     if (st == GR_OK) st = build_pull_head(g);
     cudaStreamSynchronize(g->stream);
@@ -513,11 +529,22 @@ static gr_status prepare_real(Graph *g) {
     return st;
 }
 
-static gr_status prepare_loopback(LoopGroup *grp) {
+gr_status prepare_loopback(LoopGroup *grp) {
     Graph *g0 = grp->graphs[0];
     const int P = grp->P;
-    for (int r = 0; r < P; ++r)
+    int64_t mg = 0, nig = 0;
+    uint32_t mw = 0;
+    for (int q = 0; q < P; ++q) {
+        mg += grp->graphs[q]->m;
+        nig += grp->graphs[q]->nonisolated;
+        mw = grp->graphs[q]->max_w > mw ? grp->graphs[q]->max_w : mw;
+    }
+    for (int r = 0; r < P; ++r) {
         for (int q = 0; q < P; ++q) grp->graphs[r]->sym_peer[q] = grp->graphs[q]->sym;
+        grp->graphs[r]->m_global = mg;
+        grp->graphs[r]->nonisolated_global = nig;
+        grp->graphs[r]->maxw_global = mw;
+    }
     int32_t *deg = nullptr;
     GR_CUDA(cudaMalloc((void **)&deg, (size_t)g0->block * P * sizeof(int32_t)));
     for (int q = 0; q < P; ++q) {

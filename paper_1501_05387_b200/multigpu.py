@@ -16,7 +16,8 @@ from __future__ import annotations
 import ctypes
 from typing import List, Optional
 
-from . import (DIRECTION, GR_SYMMETRIC, GR_VALIDATE, _check, _ptr, gr_bfs_opts, gr_get_run_stats, load)
+from . import (DIRECTION, GR_SYMMETRIC, GR_VALIDATE, _check, _ptr, gr_bfs_opts, gr_get_run_stats, gr_sssp_opts,
+               load)
 
 GR_KEEP_ORDER = 8
 
@@ -118,11 +119,26 @@ class PartitionedGraph:
         _check(load().gr_bfs(self.handle, int(src), dp, pp, ctypes.byref(o)))
         return depth, pred
 
+    def sssp(self, src: int, dist=None, pred=None, *, want_pred: bool = True, delta: int = 0):
+        """Collective SSSP from GLOBAL src (int32 tensor holding uint32 dist bits);
+        outputs cover the owned block; delta 0 = auto (reading A-10)."""
+        import torch
+        dev = torch.device("cuda", self.comm.device)
+        if dist is None:
+            dist = torch.empty(self.n_local, dtype=torch.int32, device=dev)
+        if pred is None and want_pred:
+            pred = torch.empty(self.n_local, dtype=torch.int32, device=dev)
+        o = gr_sssp_opts(int(delta) & 0xFFFFFFFF, 0)
+        dp, _ = _ptr(dist)
+        pp, _ = _ptr(pred)
+        _check(load().gr_sssp(self.handle, int(src), dp, pp, ctypes.byref(o)))
+        return dist, pred
+
     def run_stats(self):
         st = gr_get_run_stats(self.handle)
         recs = [st.levels[i] for i in range(st.num_records)]
         return dict(num_levels=st.num_levels, reached=st.reached, reached_edges=st.reached_edges,
-                    kernel_launches=st.kernel_launches,
+                    kernel_launches=st.kernel_launches, delta=st.delta,
                     levels=[dict(level=r.level, direction=r.direction, frontier=r.frontier,
                                  frontier_edges=r.frontier_edges, discovered=r.discovered,
                                  inspected_edges=r.inspected_edges, aux=r.aux, ns=r.ns) for r in recs])

@@ -159,3 +159,81 @@ def test_world1_nccl_comm(mg):
         comm.close()
     finally:
         dist.destroy_process_group()
+
+
+# ---- gr_sssp on a partitioned graph (psssp.cu) ------------------------------
+
+def _loopback_weighted(mg, g, P):
+    comms = mg.Comm.loopback(P)
+    parts = []
+    for r in range(P):
+        v0, v1, Rl, Cl, Wl = mg.partition_csr(g.R, g.C, P, r, W=g.W)
+        parts.append(mg.PartitionedGraph(comms[r], Rl.cuda(), Cl.cuda(), g.n, W_local=Wl.cuda()))
+    return comms, parts
+
+
+def _sssp_check(parts, g, srcs, deltas=(0,)):
+    R, C, W = g.numpy()
+    for s in srcs:
+        ref, _ = oracle.sssp(R, C, W, s)
+        for dl in deltas:
+            outs = [p.sssp(s, delta=dl) for p in parts]
+            dist = torch.cat([o[0] for o in outs]).cpu().numpy().view(np.uint32)
+            pred = torch.cat([o[1] for o in outs]).cpu().numpy()
+            bad = np.flatnonzero(dist != ref)
+            assert bad.size == 0, (len(parts), s, dl, bad[:5], dist[bad[:5]], ref[bad[:5]])
+            assert oracle.check_sssp(R, C, W, s, dist, pred) == [], (len(parts), s, dl)
+            assert sum(p.run_stats()["reached"] for p in parts) == int((ref != oracle.UINT32_MAX).sum())
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 4, 8])
+def test_loopback_sssp_rmat(mg, P):
+    """Near/far delta-stepping over P partitions (remote relaxations shipped
+    as (vertex, dist, parent) records into the owners' inboxes), every delta
+    regime: narrow bands, SPEC's ceil(mean w) = 33, one band (Bellman-Ford)."""
+    g = gg.assign_weights(gg.rmat(13, 16, seed=6), seed=2)
+    comms, parts = _loopback_weighted(mg, g, P)
+    _sssp_check(parts, g, [0] + gg.sources(g, 2), deltas=(0, 1, 8, 33, 0xFFFFFFFF))
+    _close(comms, parts)
+
+
+@pytest.mark.parametrize("P", [2, 5])
+def test_loopback_sssp_mesh_and_orkut(mg, P):
+    """High-diameter mesh (hundreds of steps, many re-splits) and the
+    orkut-like Chung-Lu shape, auto delta (A-10) and a wide band."""
+    for g in (gg.make_config("c4_road", shrink=6, weights=True), gg.make_config("c3_orkut", shrink=8, weights=True)):
+        comms, parts = _loopback_weighted(mg, g, P)
+        _sssp_check(parts, g, gg.sources(g, 1), deltas=(0, 1024))
+        _close(comms, parts)
+
+
+def test_loopback_sssp_errors_and_tiny(mg):
+    import paper_1501_05387_b200 as gr
+    g = gg.rmat(10, 8, seed=1)  # no weights
+    comms, parts = _loopback_graphs(mg, g, 2)
+    for p in parts[:1]:
+        with pytest.raises(gr.GrError) as e:
+            p.sssp(0)
+        assert e.value.status in (1, 4)
+    _close(comms, parts)
+    g = gg.assign_weights(gg.from_edges(200, [(i, i + 1) for i in range(190)] + [(195, 196)]), seed=3)
+    comms, parts = _loopback_weighted(mg, g, 4)
+    _sssp_check(parts, g, [0, 100, 199, 195], deltas=(0, 1, 0xFFFFFFFF))
+    _close(comms, parts)
+
+
+def test_world1_nccl_sssp(mg):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        comm = mg.Comm.from_torch()
+        g = gg.assign_weights(gg.kronecker(15, 16, seed=4), seed=5)
+        v0, v1, Rl, Cl, Wl = mg.partition_csr(g.R, g.C, 1, 0, W=g.W)
+        part = mg.PartitionedGraph(comm, Rl.cuda(), Cl.cuda(), g.n, W_local=Wl.cuda())
+        _sssp_check([part], g, gg.sources(g, 2), deltas=(0, 64))
+        part.close()
+        comm.close()
+    finally:
+        dist.destroy_process_group()
