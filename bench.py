@@ -73,7 +73,7 @@ def parse():
     ap.add_argument("--no-extras", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--keep-order", action="store_true",
-                    help="partitioned BFS: keep the caller's pull-list order (no gr_part_order_pull_lists)")
+                    help="partitioned BFS: keep the caller's pull-list order (GR_KEEP_ORDER)")
     ap.add_argument("--partitioned", action="store_true",
                     help="1D-partitioned BFS / SSSP over all ranks; default graph c5_kron25 (BFS) / "
                          "c3_orkut (SSSP). The default for --gpus N > 1 (BASELINE config 5)")
@@ -321,7 +321,7 @@ def run_partitioned(args, rank, world, dev):
     del g
     torch.cuda.empty_cache()
     comm = mg.Comm.from_torch(dev.index)
-    part = mg.PartitionedGraph(comm, Rl, Cl, n, W_local=Wl)
+    part = mg.PartitionedGraph(comm, Rl, Cl, n, W_local=Wl, keep_order=args.keep_order)
     del Rl, Cl, Wl
 
     def run(s, d, p):
@@ -347,12 +347,9 @@ def run_partitioned(args, rank, world, dev):
             e1.record()
             torch.cuda.synchronize()
             st = part.run_stats()
-            t = torch.tensor([e0.elapsed_time(e1), float(st["reached_edges"])], dtype=torch.float64, device=dev)
-            tm = t[:1].clone()
-            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-            dist.all_reduce(t[1:])
-            ms.append(float(tm[0]))
-            edges.append(float(t[1]))
+            t_all, e_all = metrics.reduce_over_ranks(e0.elapsed_time(e1), st["reached_edges"], *reducers(dev))
+            ms.append(t_all)
+            edges.append(e_all)
             recs.append(st)
     launches = gr.gr_kernel_launch_count() - launches0
     # end to end through the C ABI: host (pinned) outputs, host wall clock, max over ranks
@@ -654,6 +651,23 @@ def run_whole_graph(args, rank, world, dev):
         dist.destroy_process_group()
 
 
+def reducers(dev):
+    """(max, sum) of a float over the torch.distributed group (NCCL on GPUs)."""
+    import torch
+    import torch.distributed as dist
+
+    def mx(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0])
+
+    def sm(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        return float(t[0])
+    return mx, sm
+
+
 def cpu_model():
     """lscpu model name of this host (the CPU baseline's hardware)."""
     try:
@@ -783,11 +797,7 @@ def main():
     summ = metrics.summarize(edges, ms)
     edges = sum(edges)
     if world > 1:
-        t = torch.tensor([tot_ms, float(edges)], dtype=torch.float64, device=dev)
-        tmax = t.clone()
-        dist.all_reduce(tmax[:1], op=dist.ReduceOp.MAX)
-        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
-        tot_ms_all, edges_all = float(tmax[0]), float(t[1])
+        tot_ms_all, edges_all = metrics.reduce_over_ranks(tot_ms, edges, *reducers(dev))
     else:
         tot_ms_all, edges_all = tot_ms, float(edges)
     value = metrics.gteps(edges_all, tot_ms_all * 1e-3)

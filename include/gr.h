@@ -342,159 +342,6 @@ gr_status gr_graph_create_partitioned(gr_comm *c, int64_t n_global, int64_t v_be
                                       int64_t m_local, const int64_t *row_offsets, const int32_t *col_indices,
                                       const uint32_t *weights, uint32_t flags, void *cuda_stream, gr_graph **out);
 
-/* ===========================================================================
- * Multi-GPU: 1D vertex partition (the paper is single-GPU and
- * lists multi-GPU as future work). One process per GPU. Rank q of
- * P owns the contiguous vertex block [q*B, min(n, (q+1)*B)), B = 32*ceil(n/(32P))
- * (word-aligned so frontier-bitmap shards concatenate), and
- * stores the out-edges of its vertices with GLOBAL column ids. A BFS level is
- *   gr_part_bfs_expand   local push advance: owned targets are claimed here,
- *                        remote targets are culled by a per-rank "already
- *                        sent" bitmap and bucketed per owner as
- *                        (vertex, parent) int32 pairs;
- *   (exchange)           the caller moves the buckets to their owners (NCCL
- *                        all-to-all through torch.distributed, or any copy);
- *   gr_part_bfs_absorb   the owner claims received vertices against its
- *                        authoritative visited bitmap; survivors join its
- *                        next local frontier;
- *   gr_part_bfs_frontier the local next-frontier size, to be summed over
- *                        ranks (termination when the global sum is 0).
- * Depth / pred outputs cover the owned block only (index v - v_begin); pred
- * holds GLOBAL parent ids.
- * =========================================================================== */
-
-/* Creates the partition of rank `rank` out of `nparts` for a graph with
- * n_global vertices. row_offsets int64[v_end - v_begin + 1] (local rows),
- * col_indices int32[m_local] GLOBAL ids in [0, n_global). v_begin / v_end must
- * equal the 1D block of `rank` (checked). Same copy / stream / error rules as
- * gr_graph_create. */
-gr_status gr_graph_create_part(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin,
-                               int64_t v_end, int64_t m_local, const int64_t *row_offsets,
-                               const int32_t *col_indices, uint32_t flags, int device,
-                               void *cuda_stream, gr_graph **out);
-
-/* Device buffers of the exchange (valid for the graph's lifetime):
- *   send_pairs   int32[2 * nparts * block]: bucket of peer q starts at
- *                2 * q * block (pairs (vertex, parent), global ids)
- *   send_counts  int64[nparts]: pairs in each bucket after gr_part_bfs_expand
- *   recv_pairs   int32[2 * n_global]: where the caller gathers incoming pairs
- *   block        B (vertices per partition) */
-gr_status gr_part_buffers(gr_graph *g, int32_t **send_pairs, int64_t **send_counts,
-                          int32_t **recv_pairs, int64_t *block);
-
-/* Starts a partitioned BFS from GLOBAL source src (every rank calls it).
- * depth_out / pred_out: DEVICE int32[v_end - v_begin] (pred may be NULL),
- * written in place by the following level calls (host memory is rejected
- * with GR_ERR_INVALID_ARGUMENT). */
-gr_status gr_part_bfs_begin(gr_graph *g, int64_t src, int32_t *depth_out, int32_t *pred_out);
-/* Level `level` local advance; fills the send buckets and counts (device). */
-gr_status gr_part_bfs_expand(gr_graph *g, int32_t level);
-/* Claims `nrecv` received pairs (device pointer) for level `level`. */
-gr_status gr_part_bfs_absorb(gr_graph *g, int32_t level, const int32_t *recv_pairs, int64_t nrecv);
-/* Local frontier of level `level` (after expand+absorb of level-1): vertex
- * count and edge count (host outputs). */
-gr_status gr_part_bfs_frontier(gr_graph *g, int32_t level, int64_t *f, int64_t *mf);
-/* As gr_part_bfs_frontier, without a host synchronisation: enqueues on the
- * graph's stream a write of {f, m_f, overflow} to DEVICE int64 out3[3]
- * (overflow: 0 none, 1 local queue overflow, 2 a received vertex this rank
- * does not own). The caller sums out3 over ranks on the device (one NCCL
- * all-reduce) and reads the totals once per level; overflow != 0 must be
- * treated as the GR_ERR_OVERFLOW gr_part_bfs_frontier would return. Host
- * out3 is rejected with GR_ERR_INVALID_ARGUMENT. */
-gr_status gr_part_bfs_frontier_async(gr_graph *g, int32_t level, int64_t *out3);
-
-/* Dense (pull) levels of a partitioned BFS, for
- * symmetric graphs (out-lists double as in-lists):
- *   gr_part_bfs_shard  writes this rank's slice of the frontier bitmap of
- *                      `level` (block/32 words, bit i = vertex v_begin + i)
- *                      into `shard` (device);
- *   (all-gather)       the caller concatenates the shards of all ranks in
- *                      rank order into a global bitmap of nparts*block bits;
- *   gr_part_bfs_pull   bottom-up step over the owned unvisited vertices
- *                      against that global bitmap; builds the local frontier
- *                      of level+1 (no exchange needed: parents are global ids).
- * block is a multiple of 32 (block = 32*ceil(n/(32*nparts))). When the
- * frontier of `level` was built by gr_part_bfs_pull(level-1), the pull step
- * already wrote its shard (one ballot word per warp) and gr_part_bfs_shard is
- * a device copy of it; otherwise the shard is built from the local queue. */
-gr_status gr_part_bfs_shard(gr_graph *g, int32_t level, uint32_t *shard);
-gr_status gr_part_bfs_pull(gr_graph *g, int32_t level, const uint32_t *global_frontier);
-/* Optional, once after gr_graph_create_part on a symmetric partition: orders
- * each owned vertex's pull list by the GLOBAL out-degree of the neighbour,
- * descending (a sorted copy; push lists keep the caller's order), so the
- * early exit of gr_part_bfs_pull finds a frontier parent sooner (the single-GPU
- * create does the same). Results are unchanged:
- * any order of a list is the same graph. deg_global: DEVICE int32[n_global],
- * out-degree of every global vertex (the all-gather of every rank's local
- * degrees), read during the call only. Returns GR_ERR_INVALID_ARGUMENT for a
- * host pointer, a non-symmetric partition or m_local >= 2^31; synchronises the
- * graph's stream. */
-gr_status gr_part_order_pull_lists(gr_graph *g, const int32_t *deg_global);
-
-/* ===========================================================================
- * Multi-GPU SSSP over the same 1D partition. The paper's
- * near/far delta-stepping (Alg. 1; "an additional
- * filter pass between two iterations") runs per partition; the
- * caller drives the steps, exchanges the triples and reduces the counters
- * (paper_1501_05387_b200/dist.py: sssp_partitioned). Per step k:
- *   near queue non-empty (globally): it += 1;
- *     gr_part_sssp_relax(k, it, fp, thr)  local relax (owned targets: packed
- *         atomicMin dist|pred (A-9), iteration+slice stamp (A-7), near/far
- *         append); remote targets: this rank's best-shipped value per vertex
- *         is lowered by atomicMin and each improved vertex enters the bucket
- *         of its owner once per step, then its final best value is packed as
- *         a (vertex, dist, parent) int32 triple;
- *     (exchange) all-to-all of the bucket sizes, then of the triples;
- *     gr_part_sssp_absorb(k, it, fp, thr, recv, nrecv)  owner relaxes them;
- *   near queue empty everywhere:
- *     gr_part_sssp_far_min(k, fp, thr)  -> local min far distance >= thr
- *         (UINT64_MAX if none); the caller all-reduces MIN; if none: done;
- *     thr' = (floor(min / delta) + 1) * delta; it += 1;
- *     gr_part_sssp_resplit(k, it, fp, thr, thr')  far pile fp -> near queue
- *         of step k+1 and far pile fp^1, stale entries (dist < thr) dropped
- *         (A-11); then fp ^= 1;
- *   k += 1; gr_part_sssp_counts(k, fp) gives the local near size (summed by
- *   the caller) and far size.
- * Starts: thr = delta (>= 1), it = 0, fp = 0, k = 0. Ends: gr_part_sssp_end
- * writes dist (UINT32_MAX unreached) and pred (GLOBAL ids, -1 unreached,
- * pred[src] = src) of the owned block into the buffers given to begin.
- * Errors: GR_ERR_NO_WEIGHTS (partition created without weights),
- * GR_ERR_OVERFLOW (max_w * (n_global-1) may overflow uint32, or a queue
- * outgrew its capacity, reported by gr_part_sssp_counts),
- * GR_ERR_OUT_OF_RANGE (src), GR_ERR_INVALID_ARGUMENT (host outputs, bad
- * step / iteration / pile indices, thr' <= thr).
- * =========================================================================== */
-
-/* gr_graph_create_part with edge weights uint32[m_local] (host or device,
- * copied), aligned with col_indices (weights 1..64). */
-gr_status gr_graph_create_part_w(int64_t n_global, int32_t nparts, int32_t rank, int64_t v_begin,
-                                 int64_t v_end, int64_t m_local, const int64_t *row_offsets,
-                                 const int32_t *col_indices, const uint32_t *weights, uint32_t flags,
-                                 int device, void *cuda_stream, gr_graph **out);
-/* dist_out uint32[v_end - v_begin], pred_out int32[...] or NULL: DEVICE memory. */
-gr_status gr_part_sssp_begin(gr_graph *g, int64_t src, uint32_t *dist_out, int32_t *pred_out);
-/* send_triples int32[3 * nparts * block] (bucket of peer q at 3*q*block),
- * send_counts int64[nparts] (triples per bucket after relax),
- * recv_triples int32[3 * nparts * block] (where the caller gathers incoming
- * triples). Valid after gr_part_sssp_begin, for the graph's lifetime. */
-gr_status gr_part_sssp_buffers(gr_graph *g, int32_t **send_triples, int64_t **send_counts,
-                               int32_t **recv_triples, int64_t *block);
-gr_status gr_part_sssp_relax(gr_graph *g, int32_t step, int32_t it, int32_t fp, uint64_t thr);
-gr_status gr_part_sssp_absorb(gr_graph *g, int32_t step, int32_t it, int32_t fp, uint64_t thr,
-                              const int32_t *recv_triples, int64_t nrecv);
-gr_status gr_part_sssp_counts(gr_graph *g, int32_t step, int32_t fp, int64_t *near_count,
-                              int64_t *far_count);
-/* As gr_part_sssp_counts without a host synchronisation: enqueues a write of
- * {near count of step, far count of pile fp, overflow code} to DEVICE int64
- * out3[3] on the graph's stream; the caller sums it over ranks (one NCCL
- * all-reduce) and treats overflow != 0 as GR_ERR_OVERFLOW. Host out3 is
- * rejected with GR_ERR_INVALID_ARGUMENT. */
-gr_status gr_part_sssp_counts_async(gr_graph *g, int32_t step, int32_t fp, int64_t *out3);
-gr_status gr_part_sssp_far_min(gr_graph *g, int32_t step, int32_t fp, uint64_t thr, uint64_t *min_out);
-gr_status gr_part_sssp_resplit(gr_graph *g, int32_t step, int32_t it, int32_t fp, uint64_t thr_old,
-                               uint64_t thr);
-gr_status gr_part_sssp_end(gr_graph *g);
-
 #ifdef __cplusplus
 }
 #endif

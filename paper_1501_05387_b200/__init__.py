@@ -71,11 +71,7 @@ _lib = None
 EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
            "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
            "gr_get_run_stats", "gr_last_error", "gr_kernel_launch_count",
-           "gr_version", "gr_graph_create_part", "gr_part_buffers", "gr_part_bfs_begin",
-           "gr_part_bfs_expand", "gr_part_bfs_absorb", "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_order_pull_lists", "gr_part_bfs_shard",
-           "gr_part_bfs_pull", "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
-           "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts", "gr_part_sssp_counts_async", "gr_part_sssp_far_min",
-           "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank",
+           "gr_version", "gr_bc", "gr_cc", "gr_pagerank",
            "gr_comm_get_unique_id", "gr_comm_create", "gr_comm_create_loopback", "gr_comm_destroy",
            "gr_comm_info", "gr_graph_create_partitioned"]
 
@@ -108,29 +104,6 @@ def load(path: str = LIB_PATH):
     lib.gr_kernel_launch_count.restype = ctypes.c_uint64
     lib.gr_version.restype = ctypes.c_char_p
     i64, i32 = ctypes.c_int64, ctypes.c_int32
-    lib.gr_graph_create_part.argtypes = [i64, i32, i32, i64, i64, i64, p, p, ctypes.c_uint32,
-                                         ctypes.c_int, p, P(p)]
-    lib.gr_part_buffers.argtypes = [p, P(p), P(p), P(p), P(i64)]
-    lib.gr_part_bfs_begin.argtypes = [p, i64, p, p]
-    lib.gr_part_bfs_expand.argtypes = [p, i32]
-    lib.gr_part_bfs_absorb.argtypes = [p, i32, p, i64]
-    lib.gr_part_bfs_frontier.argtypes = [p, i32, P(i64), P(i64)]
-    lib.gr_part_bfs_frontier_async.argtypes = [p, i32, p]
-    lib.gr_part_order_pull_lists.argtypes = [p, p]
-    lib.gr_part_bfs_shard.argtypes = [p, i32, p]
-    lib.gr_part_bfs_pull.argtypes = [p, i32, p]
-    u64 = ctypes.c_uint64
-    lib.gr_graph_create_part_w.argtypes = [i64, i32, i32, i64, i64, i64, p, p, p, ctypes.c_uint32,
-                                           ctypes.c_int, p, P(p)]
-    lib.gr_part_sssp_begin.argtypes = [p, i64, p, p]
-    lib.gr_part_sssp_buffers.argtypes = [p, P(p), P(p), P(p), P(i64)]
-    lib.gr_part_sssp_relax.argtypes = [p, i32, i32, i32, u64]
-    lib.gr_part_sssp_absorb.argtypes = [p, i32, i32, i32, u64, p, i64]
-    lib.gr_part_sssp_counts.argtypes = [p, i32, i32, P(i64), P(i64)]
-    lib.gr_part_sssp_counts_async.argtypes = [p, i32, i32, p]
-    lib.gr_part_sssp_far_min.argtypes = [p, i32, i32, u64, P(u64)]
-    lib.gr_part_sssp_resplit.argtypes = [p, i32, i32, i32, u64, u64]
-    lib.gr_part_sssp_end.argtypes = [p]
     lib.gr_bc.argtypes = [p, p, i64, p, p]
     lib.gr_cc.argtypes = [p, p, P(i64)]
     lib.gr_pagerank.argtypes = [p, ctypes.c_double, ctypes.c_double, i32, p, P(i32)]
@@ -142,12 +115,7 @@ def load(path: str = LIB_PATH):
     lib.gr_graph_create_partitioned.argtypes = [p, i64, i64, i64, i64, p, p, p, ctypes.c_uint32, p, P(p)]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
               "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
-              "gr_get_run_stats", "gr_graph_create_part", "gr_part_buffers",
-              "gr_part_bfs_begin", "gr_part_bfs_expand", "gr_part_bfs_absorb",
-              "gr_part_bfs_frontier", "gr_part_bfs_frontier_async", "gr_part_order_pull_lists", "gr_part_bfs_shard", "gr_part_bfs_pull",
-              "gr_graph_create_part_w", "gr_part_sssp_begin", "gr_part_sssp_buffers",
-              "gr_part_sssp_relax", "gr_part_sssp_absorb", "gr_part_sssp_counts",
-              "gr_part_sssp_far_min", "gr_part_sssp_resplit", "gr_part_sssp_end", "gr_bc", "gr_cc", "gr_pagerank",
+              "gr_get_run_stats", "gr_bc", "gr_cc", "gr_pagerank",
               "gr_comm_get_unique_id", "gr_comm_create", "gr_comm_create_loopback", "gr_comm_destroy",
               "gr_comm_info", "gr_graph_create_partitioned"):
         getattr(lib, f).restype = ctypes.c_int

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgr_b200.so")
-SOURCES = ["abi.cu", "graph.cu", "bfs.cu", "sssp.cu", "partition.cu", "partition_sssp.cu", "bc.cu", "cc.cu", "pagerank.cu", "comm.cu", "pbfs.cu", "psssp.cu"]
+SOURCES = ["abi.cu", "graph.cu", "bfs.cu", "sssp.cu", "bc.cu", "cc.cu", "pagerank.cu", "comm.cu", "pbfs.cu", "psssp.cu"]
 HEADERS = ["gr_internal.cuh", "frontier.cuh", "pull.cuh", "part.cuh", os.path.join("..", "..", "include", "gr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # NCCL: the library's own communicator (gr_comm_create) links the libnccl.so.2

@@ -146,10 +146,6 @@ static gr_status bfs_args(gr_graph *h, int32_t src, const int32_t *depth_out, co
                           gr_bfs_opts *o) {
     if (!h || !depth_out) { set_error("graph or depth_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     Graph *g = (Graph *)h;
-    if (g->part) {  // a gr_graph_create_part handle: global column ids, local rows
-        set_error("gr_bfs on a step-level partition (gr_graph_create_part); use gr_part_bfs_*");
-        return GR_ERR_INVALID_ARGUMENT;
-    }
     if (src < 0 || src >= g->n) {
         set_error("src=%d not in [0, n=%lld)", src, (long long)g->n);
         return GR_ERR_OUT_OF_RANGE;
@@ -244,10 +240,6 @@ static gr_status sssp_args(gr_graph *h, int32_t src, const uint32_t *dist_out, c
                            uint64_t *delta_out) {
     if (!h || !dist_out) { set_error("graph or dist_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     Graph *g = (Graph *)h;
-    if (g->part) {
-        set_error("gr_sssp on a step-level partition (gr_graph_create_part); use gr_part_sssp_*");
-        return GR_ERR_INVALID_ARGUMENT;
-    }
     if (!g->has_w) { set_error("graph was created without weights"); return GR_ERR_NO_WEIGHTS; }
     if (src < 0 || src >= g->n) {
         set_error("src=%d not in [0, n=%lld)", src, (long long)g->n);

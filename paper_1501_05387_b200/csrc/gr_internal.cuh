@@ -157,17 +157,11 @@ struct Graph {
     int num_sms = 148;
     int nwords() const { return (int)((n + 31) / 32); }
 
-    // 1D partition (gr_graph_create_part); n = owned vertices, columns global
+    // 1D partition (gr_graph_create_partitioned); n = owned vertices, columns global
     bool part = false;
     int64_t n_global = 0, v_begin = 0, v_end = 0, block = 0;
     int nparts = 1, rank = 0;
-    uint32_t *sent = nullptr;          // [ceil(n_global/32)] remote vertices already sent
-    int32_t *send_pairs = nullptr;     // [2 * nparts * block]
-    long long *send_counts = nullptr;  // [nparts]
-    int32_t *recv_pairs = nullptr;     // [2 * n_global]
-    int32_t *part_depth = nullptr, *part_pred = nullptr;
-    uint32_t *pull_shard = nullptr;   // [block/32] frontier shard written by the last pull step
-    int32_t pull_shard_level = -1;     // the level whose frontier pull_shard holds (-1: none)
+    uint32_t *sent = nullptr;          // [ceil(n_global/32)] remote vertices already shipped (pbfs.cu)
     // partitioned graph of a gr_comm (gr_graph_create_partitioned; pbfs.cu)
     Comm *comm = nullptr;
     char *sym = nullptr;               // symmetric region (same layout on every rank)
@@ -180,13 +174,9 @@ struct Graph {
     int64_t m_global = 0, nonisolated_global = 0;
     uint32_t maxw_global = 0;
     int32_t *ps_ship = nullptr;             // [n_global] vertices shipped in the current step (psssp.cu)
-    // partitioned SSSP (partition_sssp.cu)
+    // partitioned SSSP (psssp.cu)
     unsigned long long *ps_best = nullptr;  // [n_global] best (dist<<32|pred) shipped per remote vertex
     int32_t *ps_sstamp = nullptr;           // [n_global] step of the last shipment (one per step)
-    int32_t *ps_send = nullptr;             // [3 * nparts * block] (vertex, dist, parent) triples
-    int32_t *ps_recv = nullptr;             // [3 * nparts * block]
-    uint32_t *ps_dist = nullptr;            // caller's outputs (gr_part_sssp_begin)
-    int32_t *ps_pred = nullptr;
     // betweenness centrality (bc.cu)
     void *bc_vert = nullptr;                // [n] 16-B (sigma|coef, depth) records (bc.cu BcVert)
     double *bc_sig = nullptr, *bc_delta = nullptr, *bc_buf = nullptr;

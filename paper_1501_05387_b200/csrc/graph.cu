@@ -26,8 +26,7 @@ void dev_free_all(Graph *g) {
                     (g->Ct != g->C) ? g->Ct : nullptr, g->visited, g->noin, g->fbuf[0], g->fbuf[1], g->fbuf[2],
                     g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->qr[0], g->qr[1], g->depth_buf, g->pred_buf,
                     g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev,
-                    g->sent, g->send_pairs, g->send_counts, g->recv_pairs, g->ps_best, g->ps_sstamp,
-                    g->ps_send, g->ps_recv, g->bc_vert, g->bc_sig, g->bc_delta, g->bc_buf, g->bc_cnt,
+                    g->sent, g->ps_best, g->ps_sstamp, g->bc_vert, g->bc_sig, g->bc_delta, g->bc_buf, g->bc_cnt,
                     g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph, g->ps_ship};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -68,7 +67,7 @@ __global__ void reached_kernel(int kind, const uint32_t *visited, const uint32_t
 gr_status count_reached(Graph *g, int64_t *reached, int64_t *reached_edges) {
     *reached = -1;
     *reached_edges = -1;
-    if (g->last_kind == 0 || g->part) return GR_OK;
+    if (g->last_kind == 0) return GR_OK;
     if (g->last_kind == 2 && !g->dp) return GR_OK;
     unsigned long long *d = nullptr;
     GR_CUDA(cudaMalloc(&d, 2 * sizeof(unsigned long long)));

@@ -731,6 +731,7 @@ gr_status gr_graph_create_partitioned(gr_comm *ch, int64_t n_global, int64_t v_b
                                 flags | GR_KEEP_ORDER, c->device, cuda_stream, &g, n_global);
     if (st != GR_OK) return st;
     g->comm = c;
+    g->part = true;
     g->n_global = n_global; g->v_begin = v_begin; g->v_end = v_end; g->block = block;
     g->nparts = P; g->rank = c->rank;
     g->has_w = weights != nullptr || m_local == 0;

@@ -49,3 +49,10 @@ def summarize(edges, ms):
             "median": statistics.median(per),
             "graph500_aggregate": gteps_graph500(sum(edges), sum(ms) * 1e-3),
             "graph500_harmonic_mean": harmonic_mean(per) / 2.0}
+
+
+def reduce_over_ranks(ms: float, edges: float, all_reduce_max, all_reduce_sum):
+    """Whole-job numbers of one timed region: the time is the MAX over ranks
+    (the job ends when its slowest rank does), the edges the SUM. The two
+    callables reduce a float over the process group."""
+    return all_reduce_max(float(ms)), all_reduce_sum(float(edges))

@@ -41,6 +41,24 @@ def partition_csr(R, C, nranks: int, rank: int, W=None):
     return v0, v1, (R[v0:v1 + 1] - e0).contiguous(), C[e0:e1].contiguous(), Wl
 
 
+def _nccl_unique_id() -> bytes:
+    uid = ctypes.create_string_buffer(128)
+    _check(load().gr_comm_get_unique_id(uid))
+    return uid.raw
+
+
+def broadcast_unique_id(make_id, group=None) -> bytes:
+    """Bootstrap of a gr_comm (the only job torch.distributed has here):
+    rank 0 calls make_id() for the 128-byte ncclUniqueId, every rank gets it."""
+    import torch.distributed as dist
+    obj = [make_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    uid = obj[0]
+    if not isinstance(uid, (bytes, bytearray)) or len(uid) != 128:
+        raise ValueError("unique id must be 128 bytes")
+    return bytes(uid)
+
+
 class Comm:
     """gr_comm: one (real or loopback) rank of a multi-GPU group."""
 
@@ -55,12 +73,8 @@ class Comm:
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         if device is None:
             device = torch.cuda.current_device()
-        uid = ctypes.create_string_buffer(128)
-        if rank == 0:
-            _check(load().gr_comm_get_unique_id(uid))
-        obj = [uid.raw]
-        dist.broadcast_object_list(obj, src=0, group=group)
-        buf = ctypes.create_string_buffer(obj[0], 128)
+        uid = broadcast_unique_id(_nccl_unique_id, group)
+        buf = ctypes.create_string_buffer(uid, 128)
         h = ctypes.c_void_p()
         _check(load().gr_comm_create(rank, world, buf, int(device), ctypes.byref(h)))
         return cls(h, rank, world, int(device), False)

@@ -25,22 +25,22 @@ for g in (gg.assign_weights(gg.rmat(9, 8, seed=1), seed=2), gg.assign_weights(gg
     x, _ = G.pagerank(0.85, 1e-12, 10000)
     assert np.allclose(x.cpu().numpy(), oracle.pagerank(R, C), rtol=1e-9, atol=0)
     G.close()
-# partitioned BFS and SSSP (loopback, 3 partitions)
-from paper_1501_05387_b200 import dist as grd
+# partitioned BFS and SSSP (loopback group of 3 ranks, one launch: pbfs.cu / psssp.cu)
+from paper_1501_05387_b200 import multigpu as mg
 g = gg.assign_weights(gg.rmat(9, 8, seed=1), seed=2)
 R, C, W = g.numpy()
+comms = mg.Comm.loopback(3)
 parts = []
 for r in range(3):
-    v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, 3, r)
-    parts.append(grd.GpuPartition(Rl.cuda(), Cl.cuda(), g.n, 3, r, W_local=grd.partition_weights(g.R, g.W, 3, r).cuda()))
-grp = grd.LoopbackGroup(parts)
+    v0, v1, Rl, Cl, Wl = mg.partition_csr(g.R, g.C, 3, r, W=g.W)
+    parts.append(mg.PartitionedGraph(comms[r], Rl.cuda(), Cl.cuda(), g.n, W_local=Wl.cuda()))
 for s in gg.sources(g, 2):
-    depths = [torch.empty(p.n_local, dtype=torch.int32, device="cuda") for p in parts]
-    preds = [torch.empty(p.n_local, dtype=torch.int32, device="cuda") for p in parts]
-    grp.bfs(s, depths, preds)
-    assert np.array_equal(torch.cat(depths).cpu().numpy(), oracle.bfs(R, C, s)[0])
-    grp.sssp(s, depths, preds, delta=8)
-    assert np.array_equal(torch.cat(depths).cpu().numpy().view(np.uint32), oracle.sssp(R, C, W, s)[0])
+    outs = [p.bfs(s) for p in parts]
+    assert np.array_equal(torch.cat([o[0] for o in outs]).cpu().numpy(), oracle.bfs(R, C, s)[0])
+    outs = [p.sssp(s, delta=8) for p in parts]
+    assert np.array_equal(torch.cat([o[0] for o in outs]).cpu().numpy().view(np.uint32), oracle.sssp(R, C, W, s)[0])
 for p in parts:
     p.close()
+for c in comms:
+    c.close()
 print("sanitize workload ok")

@@ -102,36 +102,36 @@ def test_c5_kron25_bfs(gr):
 
 
 def test_c5_kron25_bfs_partitioned(gr):
-    """The 1D-partitioned BFS on the full C5 graph: P = 8
-    partitions in one process (device-copy exchange) and a world-size-1 NCCL
-    group, bit-exact against the oracle."""
+    """The 1D-partitioned BFS on the full C5 graph, in
+    bench.py's configuration (collective gr_bfs on gr_graph_create_partitioned
+    graphs, one persistent kernel per rank): a loopback group of 8 ranks (one
+    launch hosts all of them) and a real world-size-1 rank over NCCL,
+    bit-exact against the oracle."""
     import os
     import socket
 
     import torch.distributed as dist
-    from paper_1501_05387_b200 import dist as grd
+    from paper_1501_05387_b200 import multigpu as mg
     g = gg.make_config("c5_kron25", device="cuda")
     R, C, _ = g.numpy()
     s = gg.sources(g, 1)[0]
     ref, _ = oracle.bfs(R, C, s, want_pred=False)
     P = 8
-    deg_global = (g.R[1:] - g.R[:-1]).to(torch.int32)
+    comms = mg.Comm.loopback(P)
     parts = []
     for r in range(P):
-        v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, P, r)
-        parts.append(grd.GpuPartition(Rl, Cl, g.n, P, r))
-        parts[-1].order_pull_lists(deg_global)
+        v0, v1, Rl, Cl, _ = mg.partition_csr(g.R, g.C, P, r)
+        parts.append(mg.PartitionedGraph(comms[r], Rl, Cl, g.n))
         del Rl, Cl
-    grp = grd.LoopbackGroup(parts)
-    depths = [torch.empty(pt.n_local, dtype=torch.int32, device="cuda") for pt in parts]
-    preds = [torch.empty(pt.n_local, dtype=torch.int32, device="cuda") for pt in parts]
-    grp.bfs(s, depths, preds, direction="auto")
-    got = torch.cat(depths).cpu().numpy()
+    outs = [p.bfs(s) for p in parts]
+    got = torch.cat([o[0] for o in outs]).cpu().numpy()
     assert np.array_equal(got, ref), int((got != ref).sum())
-    assert oracle.check_bfs(R, C, s, got, torch.cat(preds).cpu().numpy()) == []
-    for pt in parts:
-        pt.close()
-    del parts, depths, preds
+    assert oracle.check_bfs(R, C, s, got, torch.cat([o[1] for o in outs]).cpu().numpy()) == []
+    for p in parts:
+        p.close()
+    for c in comms:
+        c.close()
+    del parts, outs
     torch.cuda.empty_cache()
     sk = socket.socket()
     sk.bind(("127.0.0.1", 0))
@@ -140,20 +140,42 @@ def test_c5_kron25_bfs_partitioned(gr):
     sk.close()
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
-        v0, v1, Rl, Cl = grd.partition_csr(g.R, g.C, 1, 0)
-        part = grd.GpuPartition(Rl, Cl, g.n, 1, 0)
+        comm = mg.Comm.from_torch()
+        v0, v1, Rl, Cl, _ = mg.partition_csr(g.R, g.C, 1, 0)
+        part = mg.PartitionedGraph(comm, Rl, Cl, g.n)
         del Rl, Cl
-        ex = grd.TorchDistExchange()
-        part.order_pull_lists(grd.global_degrees(part, ex))
-        depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
-        pred = torch.empty(g.n, dtype=torch.int32, device="cuda")
-        grd.bfs_partitioned(part, ex, s, depth, pred)
+        depth, pred = part.bfs(s)
         got = depth.cpu().numpy()
         assert np.array_equal(got, ref), int((got != ref).sum())
         assert oracle.check_bfs(R, C, s, got, pred.cpu().numpy()) == []
         part.close()
+        comm.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_c3_orkut_sssp_partitioned(gr):
+    """gr_sssp on gr_graph_create_partitioned graphs (psssp.cu) on the full C3
+    graph: a loopback group of 4 ranks against the oracle's Dijkstra."""
+    from paper_1501_05387_b200 import multigpu as mg
+    g = gg.make_config("c3_orkut", device="cuda")
+    R, C, W = g.numpy()
+    s = gg.sources(g, 1)[0]
+    ref, _ = oracle.sssp(R, C, W, s, want_pred=False)
+    P = 4
+    comms = mg.Comm.loopback(P)
+    parts = []
+    for r in range(P):
+        v0, v1, Rl, Cl, Wl = mg.partition_csr(g.R, g.C, P, r, W=g.W)
+        parts.append(mg.PartitionedGraph(comms[r], Rl, Cl, g.n, W_local=Wl))
+    outs = [p.sssp(s) for p in parts]
+    got = torch.cat([o[0] for o in outs]).cpu().numpy().view(np.uint32)
+    assert np.array_equal(got, ref), int((got != ref).sum())
+    assert oracle.check_sssp(R, C, W, s, got, torch.cat([o[1] for o in outs]).cpu().numpy()) == []
+    for p in parts:
+        p.close()
+    for c in comms:
+        c.close()
 
 
 # ---- the paper's other primitives at full size (SURVEY §8(f) f3/f4) --------
