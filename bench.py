@@ -145,7 +145,7 @@ class Clocks:
 
 # ----------------------------------------------------------------- byte model
 
-def algorithmic_bytes(stats, n, prim):
+def algorithmic_bytes(stats, n, prim, packed=False):
     """SURVEY §8(d) algorithmic HBM bytes of one traversal from its per-level
     records (4-byte words; bitmap probes are L2 traffic and not counted):
       push level  12 f + 4 m_f + 12 d
@@ -160,8 +160,11 @@ def algorithmic_bytes(stats, n, prim):
             B += 12 * f + 4 * mf + 12 * d
         elif r["direction"] == 2:
             B += n / 8 + 8 * r["aux"] + 4 * ins + 8 * d + n / 8
-        elif r["direction"] == 3:
-            B += 16 * f + 8 * mf + 12 * d
+        elif r["direction"] == 3:  # C + W = 8 B per edge, or the packed (C << 7) | W word: 4 B
+            B += 16 * f + (4 if packed else 8) * mf + 12 * d
+        elif r["direction"] == 5:  # pull relax: frontier bitmap, every in-list, dist of frontier in-edges
+            m_all = stats.get("m", 0)
+            B += 4 * f + n / 8 + 16 * n + 4 * m_all + 8 * mf + 12 * d
         else:
             B += 8 * f
     return B
@@ -803,13 +806,19 @@ def main():
     value = metrics.gteps(edges_all, tot_ms_all * 1e-3)
 
     peak, peak_src = load_peaks()
-    byts = [algorithmic_bytes(r, n, args.prim) for r in recs]
+    packed = bool(G.info().packed_weights) if args.prim == "sssp" else False
+    for r in recs:
+        r["m"] = m
+    byts = [algorithmic_bytes(r, n, args.prim, packed) for r in recs]
     kname = "bfs_kernel" if args.prim == "bfs" else "sssp_kernel"
     achieved = sum(byts) / (tot_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_src,
                 "bytes_per_launch": sum(byts) / len(byts),
-                "model": "SURVEY 8(d) algorithmic bytes from per-level run stats (push 12f+4m_f+12d; "
+                "model": ("SURVEY 8(d) algorithmic bytes from per-level run stats (relax 16f+%de+12r; "
+                          "re-split 8|far|; +12n init); one launch per traversal" % (4 if packed else 8))
+                         if args.prim == "sssp" else
+                         "SURVEY 8(d) algorithmic bytes from per-level run stats (push 12f+4m_f+12d; "
                          "pull n/4+8u+4e_insp+8d; +8n init); one launch per traversal"}
 
     workload = "%s %s direction=%s" % (args.config, args.prim, args.direction)

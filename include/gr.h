@@ -105,6 +105,8 @@ typedef struct {
     uint32_t max_weight;
     int32_t device;
     int64_t device_bytes;    /* device memory currently owned by the graph      */
+    int32_t packed_weights;  /* 1: SSSP streams the packed (C << 7) | W array
+                                (n < 2^25, weights <= 127; 4 B per edge)         */
 } gr_graph_info;
 
 gr_status gr_graph_info_get(const gr_graph *g, gr_graph_info *out);
@@ -160,6 +162,13 @@ typedef struct {
     uint32_t delta;      /* near/far band width; 0 = auto; UINT32_MAX = one band
                             (Bellman-Ford-like)                                    */
     int32_t strategy;    /* as gr_bfs_opts.strategy                                */
+    int32_t direction;   /* near iterations: 0 auto, 1 push (relax the frontier's
+                            out-edges), 2 pull (every vertex takes the minimum over
+                            its in-edges from the frontier, named for
+                            SSSP in P:832-834; reading A-24). Pull needs the packed
+                            edge stream (gr_graph_info.packed_weights); otherwise
+                            push runs. Partitioned graphs: push.               */
+    double alpha;        /* auto: pull when frontier edges * alpha > m; 0 = 4     */
 } gr_sssp_opts;
 
 gr_status gr_sssp(gr_graph *g, int32_t src, uint32_t *dist_out, int32_t *pred_out,
@@ -240,6 +249,21 @@ const char *gr_version(void);
  * Synchronous: one host read per BFS level of each source.
  * =========================================================================== */
 gr_status gr_bc(gr_graph *g, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out);
+
+/* gr_bc with options: the direction of each forward level (the paper names
+ * pull as the next step for BC): push = the advance over the
+ * level queue above; pull = every undiscovered vertex sums sigma over its
+ * in-neighbours at the current depth (no atomics, no early exit). Auto picks
+ * pull when the frontier's edges exceed the undiscovered vertices' edges /
+ * alpha (reading A-24). Results are identical in every mode.
+ * gr_get_run_stats after a gr_bc: per-level records (direction, frontier,
+ * frontier edges; aux = undiscovered edges) of the LAST source's forward pass. */
+typedef struct {
+    int32_t direction;   /* 0 auto, 1 push only, 2 pull only                           */
+    double alpha;        /* auto: pull when m_f > m_u / alpha; 0 = 2                 */
+} gr_bc_opts;
+gr_status gr_bc_ex(gr_graph *g, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out,
+                   const gr_bc_opts *opts);
 
 /* ===========================================================================
  * Connected components (paper §5.4: hooking on

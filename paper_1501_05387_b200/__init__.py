@@ -43,14 +43,20 @@ class gr_bfs_opts(ctypes.Structure):
 
 
 class gr_sssp_opts(ctypes.Structure):
-    _fields_ = [("delta", ctypes.c_uint32), ("strategy", ctypes.c_int32)]
+    _fields_ = [("delta", ctypes.c_uint32), ("strategy", ctypes.c_int32), ("direction", ctypes.c_int32),
+                ("alpha", ctypes.c_double)]
+
+
+class gr_bc_opts(ctypes.Structure):
+    _fields_ = [("direction", ctypes.c_int32), ("alpha", ctypes.c_double)]
 
 
 class gr_graph_info(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("m", ctypes.c_int64), ("max_degree", ctypes.c_int64),
                 ("nonisolated", ctypes.c_int64), ("symmetric", ctypes.c_int32),
                 ("has_weights", ctypes.c_int32), ("max_weight", ctypes.c_uint32),
-                ("device", ctypes.c_int32), ("device_bytes", ctypes.c_int64)]
+                ("device", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
+                ("packed_weights", ctypes.c_int32)]
 
 
 class gr_level_stats(ctypes.Structure):
@@ -71,7 +77,7 @@ _lib = None
 EXPORTS = ["gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
            "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
            "gr_get_run_stats", "gr_last_error", "gr_kernel_launch_count",
-           "gr_version", "gr_bc", "gr_cc", "gr_pagerank",
+           "gr_version", "gr_bc", "gr_bc_ex", "gr_cc", "gr_pagerank",
            "gr_comm_get_unique_id", "gr_comm_create", "gr_comm_create_loopback", "gr_comm_destroy",
            "gr_comm_info", "gr_graph_create_partitioned"]
 
@@ -105,6 +111,7 @@ def load(path: str = LIB_PATH):
     lib.gr_version.restype = ctypes.c_char_p
     i64, i32 = ctypes.c_int64, ctypes.c_int32
     lib.gr_bc.argtypes = [p, p, i64, p, p]
+    lib.gr_bc_ex.argtypes = [p, p, i64, p, p, P(gr_bc_opts)]
     lib.gr_cc.argtypes = [p, p, P(i64)]
     lib.gr_pagerank.argtypes = [p, ctypes.c_double, ctypes.c_double, i32, p, P(i32)]
     lib.gr_comm_get_unique_id.argtypes = [p]
@@ -115,7 +122,7 @@ def load(path: str = LIB_PATH):
     lib.gr_graph_create_partitioned.argtypes = [p, i64, i64, i64, i64, p, p, p, ctypes.c_uint32, p, P(p)]
     for f in ("gr_graph_create", "gr_graph_destroy", "gr_graph_set_stream", "gr_graph_info_get",
               "gr_bfs", "gr_sssp", "gr_bfs_async", "gr_sssp_async", "gr_graph_sync",
-              "gr_get_run_stats", "gr_bc", "gr_cc", "gr_pagerank",
+              "gr_get_run_stats", "gr_bc", "gr_bc_ex", "gr_cc", "gr_pagerank",
               "gr_comm_get_unique_id", "gr_comm_create", "gr_comm_create_loopback", "gr_comm_destroy",
               "gr_comm_info", "gr_graph_create_partitioned"):
         getattr(lib, f).restype = ctypes.c_int
@@ -263,20 +270,22 @@ class Graph:
         return depth, pred
 
     def sssp(self, src: int, dist=None, pred=None, *, want_pred: bool = True,
-             delta: int = 0, strategy="auto", asynchronous: bool = False):
+             delta: int = 0, strategy="auto", direction="auto", alpha: float = 0.0,
+             asynchronous: bool = False):
         import torch
         dev = torch.device("cuda", self.device)
         if dist is None:
             dist = torch.empty(self.n, dtype=torch.int32, device=dev)  # uint32 bits
         if pred is None and want_pred:
             pred = torch.empty(self.n, dtype=torch.int32, device=dev)
-        o = gr_sssp_opts(int(delta) & 0xFFFFFFFF, STRATEGY.get(strategy, strategy))
+        o = gr_sssp_opts(int(delta) & 0xFFFFFFFF, STRATEGY.get(strategy, strategy),
+                         DIRECTION.get(direction, direction), float(alpha))
         dp, _ = _ptr(dist)
         pp, _ = _ptr(pred)
         (gr_sssp_async if asynchronous else gr_sssp)(self.handle, src, dp, pp, o)
         return dist, pred
 
-    def bc(self, sources, bc=None, sigma=None):
+    def bc(self, sources, bc=None, sigma=None, direction="auto", alpha: float = 0.0):
         """Betweenness centrality (Brandes): bc[v] = sum over the
         given sources s of the dependency delta_s(v) (fp64; no halving -- for
         a symmetric graph over all sources Brandes's value is bc / 2)."""
@@ -287,7 +296,9 @@ class Graph:
             bc = torch.empty(self.n, dtype=torch.float64, device=torch.device("cuda", self.device))
         bp, _ = _ptr(bc)
         sp, _ = _ptr(sigma)
-        _check(load().gr_bc(self.handle, src.ctypes.data_as(ctypes.c_void_p), int(src.size), bp, sp))
+        o = gr_bc_opts(DIRECTION.get(direction, direction), float(alpha))
+        _check(load().gr_bc_ex(self.handle, src.ctypes.data_as(ctypes.c_void_p), int(src.size), bp, sp,
+                               ctypes.byref(o)))
         return bc
 
     def cc(self, comp=None):

@@ -40,8 +40,8 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
 bool ptr_on_device(const void *p);
 gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr_bfs_opts &o,
                   int *launches);
-gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta,
-                   int *launches);
+gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta, int32_t direction,
+                   double alpha, int *launches);
 gr_status pbfs_collective(Graph *g, int64_t src, int32_t *depth_out, int32_t *pred_out, const gr_bfs_opts &o);
 gr_status psssp_collective(Graph *g, int64_t src, uint32_t *dist_out, int32_t *pred_out, uint32_t delta);
 
@@ -116,6 +116,7 @@ gr_status gr_graph_info_get(const gr_graph *h, gr_graph_info *out) {
     out->n = g->n; out->m = g->m; out->max_degree = g->max_deg; out->nonisolated = g->nonisolated;
     out->symmetric = g->symmetric; out->has_weights = g->has_w; out->max_weight = g->max_w;
     out->device = g->device; out->device_bytes = g->bytes;
+    out->packed_weights = g->CW != nullptr;
     return GR_OK;
 }
 
@@ -237,7 +238,7 @@ gr_status gr_bfs_async(gr_graph *h, int32_t src, int32_t *depth_out, int32_t *pr
 }
 
 static gr_status sssp_args(gr_graph *h, int32_t src, const uint32_t *dist_out, const gr_sssp_opts *opts,
-                           uint64_t *delta_out) {
+                           uint64_t *delta_out, gr_sssp_opts *o_out) {
     if (!h || !dist_out) { set_error("graph or dist_out is NULL"); return GR_ERR_INVALID_ARGUMENT; }
     Graph *g = (Graph *)h;
     if (!g->has_w) { set_error("graph was created without weights"); return GR_ERR_NO_WEIGHTS; }
@@ -251,7 +252,11 @@ static gr_status sssp_args(gr_graph *h, int32_t src, const uint32_t *dist_out, c
     }
     gr_sssp_opts o{};
     if (opts) o = *opts;
-    if (o.strategy < 0 || o.strategy > 2) { set_error("invalid gr_sssp_opts"); return GR_ERR_INVALID_ARGUMENT; }
+    if (o.strategy < 0 || o.strategy > 2 || o.direction < 0 || o.direction > 2 || o.alpha < 0) {
+        set_error("invalid gr_sssp_opts");
+        return GR_ERR_INVALID_ARGUMENT;
+    }
+    *o_out = o;
     uint64_t delta = o.delta;
     if (delta == 0) {
         // auto delta (reading A-10): dense low-diameter graphs want narrow
@@ -291,7 +296,8 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
         return psssp_collective(g, src, dist_out, pred_out, o.delta);
     }
     uint64_t delta = 0;
-    gr_status st = sssp_args(h, src, dist_out, opts, &delta);
+    gr_sssp_opts so{};
+    gr_status st = sssp_args(h, src, dist_out, opts, &delta, &so);
     if (st != GR_OK) return st;
     Graph *g = (Graph *)h;
     if (g->pending && (st = gr_graph_sync(h)) != GR_OK) return st;
@@ -308,7 +314,7 @@ gr_status gr_sssp(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *pred_ou
         pred = g->pred_buf;
     }
     int launches = 0;
-    if ((st = run_sssp(g, src, dist, pred, delta, &launches)) != GR_OK) return st;
+    if ((st = run_sssp(g, src, dist, pred, delta, so.direction, so.alpha, &launches)) != GR_OK) return st;
     if (!dev_dist)
         GR_CUDA(cudaMemcpyAsync(dist_out, dist, g->n * sizeof(uint32_t), cudaMemcpyDeviceToHost, g->stream));
     if (pred_out && !dev_pred)
@@ -327,7 +333,8 @@ gr_status gr_sssp_async(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *p
         return GR_ERR_INVALID_ARGUMENT;
     }
     uint64_t delta = 0;
-    gr_status st = sssp_args(h, src, dist_out, opts, &delta);
+    gr_sssp_opts so{};
+    gr_status st = sssp_args(h, src, dist_out, opts, &delta, &so);
     if (st != GR_OK) return st;
     Graph *g = (Graph *)h;
     if (!ptr_on_device(dist_out) || (pred_out && !ptr_on_device(pred_out))) {
@@ -335,7 +342,7 @@ gr_status gr_sssp_async(gr_graph *h, int32_t src, uint32_t *dist_out, int32_t *p
         return GR_ERR_INVALID_ARGUMENT;
     }
     int launches = 0;
-    if ((st = run_sssp(g, src, dist_out, pred_out, delta, &launches)) != GR_OK) return st;
+    if ((st = run_sssp(g, src, dist_out, pred_out, delta, so.direction, so.alpha, &launches)) != GR_OK) return st;
     GR_CUDA(cudaGetLastError());
     g->last_launches = launches;
     g->last_delta = (uint32_t)(delta > 0xFFFFFFFFull ? 0xFFFFFFFFull : delta);

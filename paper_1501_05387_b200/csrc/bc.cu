@@ -53,6 +53,8 @@ struct BcArgs {
     int64_t n;
     const int64_t *R;
     const int32_t *C;
+    const int64_t *Rt;         // in-lists (the CSR itself when symmetric): pull levels
+    const int32_t *Ct;
     BcVert *bv;
     double *delta;
     int32_t *qv;               // all levels back to back
@@ -188,6 +190,89 @@ __global__ void __launch_bounds__(kBcBlock) bc_fwd_kernel(BcArgs a, int L, int64
     app.finish();
 }
 
+// Pull (bottom-up) forward level L -> L+1 (paper P:804-834, named for BC in
+// "more sophisticated BC and SSSP implementations could benefit
+// from it"): every unvisited vertex v with in-edges sums sigma over its
+// in-neighbours at depth L -- sigma[v] = sum over (u,v) in E, d[u] = L of
+// sigma[u], Brandes's forward recurrence read from the receiver's side. No
+// early exit (every parent counts) but no atomics: v is owned by one lane
+// (lists of <= kBcPullLane edges) or one warp (longer lists, 32 edges a step
+// with a warp reduction). Found vertices join the level-(L+1) queue.
+constexpr int64_t kBcPullLane = 8;
+
+__global__ void __launch_bounds__(kBcBlock) bc_fwd_pull_kernel(BcArgs a, int L, int64_t off, int64_t f) {
+    __shared__ int32_t s_v[kBcWarps][kBcStage];
+    __shared__ int32_t s_d[kBcWarps][kBcStage];
+    __shared__ int64_t s_r[kBcWarps][kBcStage];
+    const int wib = threadIdx.x >> 5;
+    const unsigned l = lane_id();
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.cnt[L + 2] = 0ull;  // read by level L+1
+    BcAppender app;
+    app.sv = s_v[wib]; app.sd = s_d[wib]; app.sr = s_r[wib]; app.cnt = 0; app.S = a.S;
+    app.cap = a.n - (off + f);
+    app.overflow = a.cnt + a.n + 2;
+    app.qv = a.qv + off + f;
+    app.qo = a.qo + off + f;
+    app.qr = a.qr + off + f;
+    app.counter = a.cnt + L + 1;
+    const unsigned long long pol = policy_evict_first();
+    for (int64_t base = gw * 32; base < a.n; base += nw * 32) {
+        const int64_t v = base + l;
+        int64_t b = 0, e = 0;
+        bool cand = false;
+        if (v < a.n && __ldcg(&a.bv[v].depth) == -1) {
+            b = a.Rt[v];
+            e = a.Rt[v + 1];
+            cand = e > b;
+        }
+        double sum = 0.0;
+        const bool lane_list = cand && e - b <= kBcPullLane;
+        if (lane_list) {  // short list: this lane, 4 neighbour loads then 4 record loads in flight
+            for (int64_t x = b; x < e; x += 4) {
+                int32_t u[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) u[j] = x + j < e ? ld_stream(a.Ct + x + j, pol) : -1;
+                double2 r[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    r[j] = u[j] >= 0 ? __ldcg(reinterpret_cast<const double2 *>(a.bv + u[j])) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (u[j] >= 0 && (int32_t)(__double_as_longlong(r[j].y) & 0xffffffffll) == L) sum += r[j].x;
+            }
+        }
+        unsigned lm = __ballot_sync(0xffffffffu, cand && !lane_list);
+        while (lm) {  // long lists: the whole warp, one list at a time
+            const int ld = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const int64_t lb = __shfl_sync(0xffffffffu, b, ld), le = __shfl_sync(0xffffffffu, e, ld);
+            double part = 0.0;
+            for (int64_t x = lb + l; x < le; x += 32) {
+                const int32_t u = ld_stream(a.Ct + x, pol);
+                const double2 r = __ldcg(reinterpret_cast<const double2 *>(a.bv + u));
+                if ((int32_t)(__double_as_longlong(r.y) & 0xffffffffll) == L) part += r.x;
+            }
+            part = warp_sum<double>(part);
+            if ((int)l == ld) sum = part;
+        }
+        const bool found = cand && sum > 0.0;
+        int64_t deg = 0, rs = 0;
+        if (found) {
+            BcVert x;
+            x.val = sum;
+            x.depth = L + 1;
+            x.pad = 0;
+            a.bv[v] = x;
+            rs = a.R[v];
+            deg = a.R[v + 1] - rs;
+        }
+        app.push(found, (int32_t)v, deg, rs);
+    }
+    app.finish();
+}
+
 __global__ void __launch_bounds__(kBcBlock) bc_bwd_kernel(BcArgs a, int L, int64_t off, int64_t f, int64_t mf) {
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -215,8 +300,12 @@ using namespace gr;
 
 extern "C" {
 
-gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out) {
+gr_status gr_bc_ex(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out,
+                   const gr_bc_opts *opts) {
     Graph *g = (Graph *)h;
+    gr_bc_opts o = opts ? *opts : gr_bc_opts{};
+    if (o.direction < 0 || o.direction > 2 || o.alpha < 0) { set_error("invalid gr_bc_opts"); return GR_ERR_INVALID_ARGUMENT; }
+    const double alpha = o.alpha > 0 ? o.alpha : 2.0;
     if (!g || !bc_out || nsrc < 0 || (nsrc > 0 && !sources)) {
         set_error("graph / bc_out / sources is NULL or nsrc < 0");
         return GR_ERR_INVALID_ARGUMENT;
@@ -245,7 +334,7 @@ gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_ou
         bc = g->bc_buf;
     }
     BcArgs a;
-    a.n = n; a.R = g->R; a.C = g->C;
+    a.n = n; a.R = g->R; a.C = g->C; a.Rt = g->Rt; a.Ct = g->Ct;
     a.bv = (BcVert *)g->bc_vert; a.delta = g->bc_delta;
     double *sig = nullptr;  // sigma of the last source, saved before the backward pass overwrites it
     if (sigma_out && nsrc > 0) {
@@ -270,6 +359,7 @@ gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_ou
         off.assign(1, 0);
         fs.clear();
         mfs.clear();
+        int64_t m_u = g->m;  // out-edges of vertices not yet discovered (their in-lists on symmetric graphs)
         for (int L = 0;; ++L) {  // forward phase: BFS + sigma (one host read per level)
             unsigned long long qp = 0;
             GR_CUDA(cudaMemcpyAsync(&qp, a.cnt + L, sizeof(qp), cudaMemcpyDeviceToHost, s));
@@ -278,7 +368,19 @@ gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_ou
             if (f == 0) break;
             fs.push_back(f);
             mfs.push_back(mf);
-            bc_fwd_kernel<<<grid, kBcBlock, 0, s>>>(a, L, off[L], f, mf);
+            m_u -= mf;
+            // direction (A-24): pull when the frontier's edges exceed the
+            // unvisited vertices' edges / alpha (no early exit in a BC pull:
+            // it reads every unvisited list in full, hence a small alpha)
+            const bool pull = o.direction == 2 || (o.direction == 0 && (double)mf > (double)m_u / alpha);
+            if (pull) bc_fwd_pull_kernel<<<grid, kBcBlock, 0, s>>>(a, L, off[L], f);
+            else bc_fwd_kernel<<<grid, kBcBlock, 0, s>>>(a, L, off[L], f, mf);
+            if (i == nsrc - 1 && L < kMaxStatRecords) {  // per-level records of the last source
+                gr_level_stats rec{};
+                rec.level = L; rec.direction = pull ? 2 : 1; rec.frontier = f; rec.frontier_edges = mf;
+                rec.aux = m_u;
+                g->stats_host[L] = rec;
+            }
             ++launches;
             off.push_back(off[L] + f);
         }
@@ -310,8 +412,13 @@ gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_ou
     count_launch(launches);
     g->last_launches = launches;
     g->stats_levels = levels_total;
-    g->stats_records = -1;  // no per-level records for BC
+    g->stats_records = nsrc > 0 ? (int)(fs.size() < (size_t)kMaxStatRecords ? fs.size() : kMaxStatRecords) : 0;
+    g->last_kind = 0;  // run totals are not counted for BC
     return GR_OK;
+}
+
+gr_status gr_bc(gr_graph *h, const int32_t *sources, int64_t nsrc, double *bc_out, double *sigma_out) {
+    return gr_bc_ex(h, sources, nsrc, bc_out, sigma_out, nullptr);
 }
 
 }  // extern "C"

@@ -116,6 +116,8 @@ struct Graph {
     int64_t *R = nullptr;         // [n+1]
     int32_t *C = nullptr;         // [m]
     uint32_t *W = nullptr;        // [m] or null
+    uint32_t *CW = nullptr;       // [m] packed (C << 7) | W for SSSP, or null (graph.cu)
+    uint32_t *CWt = nullptr;      // [m] packed in-lists (u << 7) | w(u,v) at Rt: pull SSSP (lazy)
     int64_t *Rt = nullptr;        // CSC (== R when symmetric)
     int32_t *Ct = nullptr;
     int2 *ph = nullptr;           // pull head: {Ct[Rt[v]] or -1, in-degree} (pull steps, pull.cuh)
@@ -191,6 +193,7 @@ struct Graph {
 
 gr_status dev_alloc(Graph *g, void **p, size_t bytes);
 gr_status count_reached(Graph *g, int64_t *reached, int64_t *reached_edges);
+gr_status build_pull_weights(Graph *g);
 void dev_free_all(Graph *g);
 
 // ---------------------------------------------------------------- device helpers

@@ -27,7 +27,7 @@ void dev_free_all(Graph *g) {
                     g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->qr[0], g->qr[1], g->depth_buf, g->pred_buf,
                     g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev,
                     g->sent, g->ps_best, g->ps_sstamp, g->bc_vert, g->bc_sig, g->bc_delta, g->bc_buf, g->bc_cnt,
-                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph, g->ps_ship};
+                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph, g->ps_ship, g->CW, g->CWt};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (g->stats_host) cudaFreeHost(g->stats_host);
@@ -230,6 +230,45 @@ done:
     return st;
 }
 
+// Packed SSSP edge stream: CW[e] = (C[e] << 7) | W[e] (sssp.cu RelaxOpT<true>).
+__global__ void pack_cw_kernel(const int32_t *C, const uint32_t *W, int64_t m, uint32_t *CW) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = tid; e < m; e += nt) CW[e] = ((uint32_t)C[e] << 7) | W[e];
+}
+
+// Weighted in-lists for pull SSSP steps (sssp.cu): CWt[Rt[v] ..) holds
+// (u << 7) | w(u, v) for every edge (u, v) -- the transpose of CW, so it is
+// right for any weights (a symmetric structure need not carry symmetric
+// weights). One warp per source row; the order inside an in-list is free.
+__global__ void scatter_cwt_kernel(const int64_t *R, const uint32_t *CW, int64_t n,
+                                   unsigned long long *cursor, uint32_t *CWt) {
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const unsigned l = threadIdx.x & 31;
+    for (int64_t u = gw; u < n; u += nw)
+        for (int64_t e = R[u] + l; e < R[u + 1]; e += 32) {
+            const uint32_t x = CW[e];
+            const unsigned long long p = atomicAdd(cursor + (x >> 7), 1ull);
+            CWt[p] = ((uint32_t)u << 7) | (x & 127u);
+        }
+}
+
+gr_status build_pull_weights(Graph *g) {
+    if (g->CWt || !g->CW) return GR_OK;  // no packed edge stream: no pull SSSP
+    gr_status st = dev_alloc(g, (void **)&g->CWt, g->m * sizeof(uint32_t) + 16);
+    if (st != GR_OK) return st;
+    unsigned long long *cur = nullptr;
+    GR_CUDA(cudaMalloc((void **)&cur, (g->n + 1) * sizeof(unsigned long long)));
+    GR_CUDA(cudaMemcpyAsync(cur, g->Rt, g->n * sizeof(int64_t), cudaMemcpyDeviceToDevice, g->stream));
+    scatter_cwt_kernel<<<g->num_sms * 8, 256, 0, g->stream>>>(g->R, g->CW, g->n, cur, g->CWt);
+    count_launch();
+    cudaError_t e = cudaStreamSynchronize(g->stream);
+    cudaFree(cur);
+    if (e != cudaSuccess) return cuda_fail(e, "scatter_cwt_kernel", __FILE__, __LINE__);
+    return GR_OK;
+}
+
 // Pull head (pull.cuh): per vertex its first in-list entry -- the highest-
 // degree in-neighbour once lists are ordered -- and its in-degree, so a pull
 // step resolves most candidates with one 8-byte load per vertex instead of
@@ -405,6 +444,15 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
         TRY(dev_alloc(g, (void **)&g->qr[i], 2 * n * sizeof(int64_t)));
     }
     if (ncols == n) TRY(build_pull_head(g));  // partitions: after the global list order (pbfs.cu)
+    // SSSP edge stream with the weight packed into the column word (4 bytes per
+    // relaxed edge instead of 8): ids below 2^25 and weights <= 127 (the
+    // paper's are integers 1..64)
+    if (W && m > 0 && ncols < (1ll << 25) && g->max_w <= 127 && env_int("GR_PACK_W", 1)) {
+        TRY(dev_alloc(g, (void **)&g->CW, m * sizeof(uint32_t) + 16));
+        pack_cw_kernel<<<blocks, 256, 0, s>>>(g->C, g->W, m, g->CW);
+        count_launch();
+        TRYC(cudaGetLastError());
+    }
     g->pack_shift = bits_for(2 * n + 1);
     TRY(dev_alloc(g, (void **)&g->ctl, sizeof(Ctl)));
     TRYC(cudaMemsetAsync(g->ctl, 0, sizeof(Ctl), s));

@@ -46,6 +46,7 @@ struct SRank {
     const int64_t *R;
     const int32_t *C;            // GLOBAL ids
     const uint32_t *W;
+    const uint32_t *CW;          // packed (C << 7) | W, or null
     unsigned long long *dp;      // [n_local] (dist << 32) | global pred (A-9)
     int32_t *stamp;              // [n_local] RemoveRedundant stamp (A-7)
     unsigned long long *best;    // [n_global] best value shipped to the owner (A-21)
@@ -89,6 +90,7 @@ __device__ __forceinline__ int sp_relax(const SRank &a, int64_t lv, unsigned lon
     return far ? 2 : 1;
 }
 
+template <bool kPacked>  // kPacked: the edge stream is (C << 7) | W (graph.cu), 4 B per edge
 struct PSRelaxOp {
     const SRank *a;
     uint64_t thr;
@@ -105,18 +107,25 @@ struct PSRelaxOp {
     __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *du,
                                           const int32_t *dst, const T5 *x) {
         uint32_t w[U];
+        int32_t vv[U];
         unsigned long long cur[U];
         // weight loads and pre-check probes of all U edges before any atomic
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            w[u] = ok[u] ? ld_stream(a->W + x[u], pol_stream) : 0u;
-            const int64_t lv = (int64_t)dst[u] - a->v_begin;
+            if constexpr (kPacked) {
+                vv[u] = (int32_t)((uint32_t)dst[u] >> 7);
+                w[u] = (uint32_t)dst[u] & 127u;
+            } else {
+                vv[u] = dst[u];
+                w[u] = ok[u] ? ld_stream(a->W + x[u], pol_stream) : 0u;
+            }
+            const int64_t lv = (int64_t)vv[u] - a->v_begin;
             const bool owned = lv >= 0 && lv < a->n_local;
-            cur[u] = ok[u] ? ld_probe(owned ? a->dp + lv : a->best + dst[u], pol) : 0ull;
+            cur[u] = ok[u] ? ld_probe(owned ? a->dp + lv : a->best + vv[u], pol) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int32_t v = dst[u];
+            const int32_t v = vv[u];
             const int64_t lv = (int64_t)v - a->v_begin;
             const bool owned = lv >= 0 && lv < a->n_local;
             const unsigned long long nd = du[u] + w[u];
@@ -160,7 +169,7 @@ struct SSmem {
 constexpr int kSBlock = 512;
 constexpr int kSMinB = 2;
 
-template <int kBlk, int kMinB>
+template <int kBlk, int kMinB, bool kPacked>
 __global__ void __launch_bounds__(kBlk, kMinB) psssp_kernel(const __grid_constant__ PSsspArgs A) {
     constexpr int kNW = kBlk / kWarp;
     __shared__ SSmem<kNW> sm;
@@ -283,9 +292,9 @@ __global__ void __launch_bounds__(kBlk, kMinB) psssp_kernel(const __grid_constan
             ++it;
             farq.qv = a.far[fp];
             farq.counter = &a.ctl->far_count[fp];
-            PSRelaxOp op{&a, thr, 2 * it, k, &nearq, &farq, &a.ctl->reached, pol, pol_stream, 0ull};
+            PSRelaxOp<kPacked> op{&a, thr, 2 * it, k, &nearq, &farq, &a.ctl->reached, pol, pol_stream, 0ull};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.qr[k & 1], f_loc, mf_loc};
-            expand_lb(fr, a.C, gw, nw, op, &cur.work, 4);
+            expand_lb(fr, kPacked ? reinterpret_cast<const int32_t *>(a.CW) : a.C, gw, nw, op, &cur.work, 4);
             nimp = op.nimp;
             nearq.finish_cta(sm.wsum);
             farq.finish_cta(sm.wsum);
@@ -459,7 +468,7 @@ static void fill_srank(Graph *g, SRank &r, uint32_t *dist, int32_t *pred) {
     r.rank = g->comm->rank;
     r.S = g->pack_shift;
     r.n_local = g->n; r.v_begin = g->v_begin;
-    r.R = g->R; r.C = g->C; r.W = g->W;
+    r.R = g->R; r.C = g->C; r.W = g->W; r.CW = g->CW;
     r.dp = g->dp; r.stamp = g->stamp; r.best = g->ps_best; r.sstamp = g->ps_sstamp; r.ship = g->ps_ship;
     for (int i = 0; i < 2; ++i) {
         r.qv[i] = g->qv[i]; r.qo[i] = g->qo[i]; r.qr[i] = g->qr[i]; r.far[i] = g->farq[i];
@@ -496,7 +505,10 @@ static gr_status launch_psssp(Graph **gs, int k, int64_t src, uint32_t **dist, i
     A.off_sinbox[0] = Ly.sinbox[0];
     A.off_sinbox[1] = Ly.sinbox[1];
     A.inbox_cap = Ly.inbox_cap;
-    const void *fn = (const void *)psssp_kernel<kSBlock, kSMinB>;
+    bool packed = true;
+    for (int i = 0; i < k; ++i) packed = packed && gs[i]->CW != nullptr;
+    const void *fn = packed ? (const void *)psssp_kernel<kSBlock, kSMinB, true>
+                            : (const void *)psssp_kernel<kSBlock, kSMinB, false>;
     int per_sm = 0;
     GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kSBlock, 0));
     if (per_sm < 1) { set_error("psssp_kernel cannot be resident"); return GR_ERR_CUDA; }

@@ -19,6 +19,12 @@ struct SsspArgs {
     const int64_t *R;
     const int32_t *C;
     const uint32_t *W;
+    const uint32_t *CW;       // packed (C << 7) | W, or null
+    const int64_t *Rt;        // in-list offsets (== R when symmetric)
+    const uint32_t *CWt;      // packed weighted in-lists (u << 7) | w(u,v), or null: no pull steps
+    uint32_t *fb;             // pull steps: bitmap of the near frontier [ceil(n/32)]
+    int32_t direction;        // 0 auto, 1 push, 2 pull (near iterations; reading A-24)
+    double alpha;             // auto: pull when m_f * alpha > m
     unsigned long long *dp;   // (dist << 32) | pred
     int32_t *stamp;
     int32_t *qv[2];
@@ -60,7 +66,11 @@ struct SsspSmem {
 };
 
 // Fused advance + compute + filter of one near iteration (a10).
-struct RelaxOp {
+// kPacked: the advance streams the packed edge array CW[e] = (C[e] << 7) | W[e]
+// (graph.cu; n < 2^25, weights <= 127 -- the paper's are 1..64)
+// instead of C and W: 4 bytes per relaxed edge instead of 8.
+template <bool kPacked>
+struct RelaxOpT {
     unsigned long long *dp;
     int32_t *stamp;
     const uint32_t *W;
@@ -84,17 +94,24 @@ struct RelaxOp {
                                           const int32_t *dst, const T5 *x) {
         unsigned long long cur[U];
         uint32_t w[U];
+        int32_t vv[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            if constexpr (sizeof(T5) == 8) w[u] = ok[u] ? ld_stream(W + x[u], pol_stream) : 0u;
-            else w[u] = (uint32_t)x[u];
-            cur[u] = ok[u] ? ld_probe(dp + dst[u], pol_keep) : 0ull;
+            if constexpr (kPacked) {
+                vv[u] = (int32_t)((uint32_t)dst[u] >> 7);
+                w[u] = (uint32_t)dst[u] & 127u;
+            } else {
+                vv[u] = dst[u];
+                if constexpr (sizeof(T5) == 8) w[u] = ok[u] ? ld_stream(W + x[u], pol_stream) : 0u;
+                else w[u] = (uint32_t)x[u];
+            }
+            cur[u] = ok[u] ? ld_probe(dp + vv[u], pol_keep) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             bool to_near = false, to_far = false;
             int64_t deg = 0, rs = 0;
-            const int32_t v = dst[u];
+            const int32_t v = vv[u];
             const unsigned long long nd = du[u] + w[u];
             if (ok[u] && nd < (cur[u] >> 32)) {
                 const unsigned long long pk = (nd << 32) | (unsigned int)src[u];
@@ -115,13 +132,89 @@ struct RelaxOp {
     }
 };
 
+// Pull (bottom-up) near iteration (the paper names SSSP as a next
+// user of pull; reading A-24): the near frontier as a bitmap, and
+// every vertex v takes min over its in-edges (u, v) with u in the frontier of
+// dist[u] + w(u, v) -- the same relaxations as the push step, computed at
+// the receiver, so dp[v] needs no atomic (v is owned by one lane, or by one
+// warp for lists longer than kSsspPullLane). An improved v joins the near
+// queue (nd < thr) or the far pile, once (no stamp race: one owner).
+constexpr int64_t kSsspPullLane = 8;
+
+template <class App>
+__device__ __forceinline__ unsigned long long sssp_pull_step(const SsspArgs &a, uint64_t thr, int32_t key_near,
+                                                             int64_t gw, int64_t nw, App &nearq, App &farq,
+                                                             unsigned long long pol) {
+    const unsigned l = lane_id();
+    unsigned long long nimp = 0;
+    const unsigned long long pol_s = policy_evict_first();
+    auto relax_in = [&](uint32_t x, unsigned long long &best) {  // one in-edge, packed (u << 7) | w
+        const int32_t u = (int32_t)(x >> 7);
+        if ((a.fb[u >> 5] >> (u & 31)) & 1u) {
+            const unsigned long long du = ld_probe(a.dp + u, pol) >> 32;
+            const unsigned long long cand = ((du + (x & 127u)) << 32) | (unsigned)u;
+            best = cand < best ? cand : best;
+        }
+    };
+    for (int64_t base = gw * 32; base < a.n; base += nw * 32) {
+        const int64_t v = base + l;
+        int64_t b = 0, e = 0;
+        if (v < a.n) { b = a.Rt[v]; e = a.Rt[v + 1]; }
+        unsigned long long best = ~0ull;  // (nd << 32) | parent: smallest nd, then smallest parent (A-9)
+        const bool lane_list = e > b && e - b <= kSsspPullLane;
+        if (lane_list) {
+            for (int64_t x0 = b; x0 < e; x0 += 4) {
+                uint32_t xx[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) xx[j] = x0 + j < e ? ld_stream(a.CWt + x0 + j, pol_s) : 0xffffffffu;
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (x0 + j < e) relax_in(xx[j], best);
+            }
+        }
+        unsigned lm = __ballot_sync(0xffffffffu, e - b > kSsspPullLane);
+        while (lm) {
+            const int ld = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const int64_t lb = __shfl_sync(0xffffffffu, b, ld), le = __shfl_sync(0xffffffffu, e, ld);
+            unsigned long long part = ~0ull;
+            for (int64_t x = lb + l; x < le; x += 32) relax_in(ld_stream(a.CWt + x, pol_s), part);
+#pragma unroll
+            for (int sh = 16; sh > 0; sh >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, part, sh);
+                part = o < part ? o : part;
+            }
+            if ((int)l == ld) best = part;
+        }
+        bool to_near = false, to_far = false;
+        int64_t deg = 0, rs = 0;
+        if (best != ~0ull) {
+            const unsigned long long cur = ld_probe(a.dp + v, pol);
+            if ((best >> 32) < (cur >> 32)) {
+                a.dp[v] = best;  // v's owner: a plain 64-bit store
+                const bool far = (best >> 32) >= thr;
+                a.stamp[v] = key_near + (far ? 1 : 0);
+                if (far) to_far = true;
+                else { to_near = true; rs = a.R[v]; deg = a.R[v + 1] - rs; }
+                ++nimp;
+            }
+        }
+        nearq.push(to_near && deg > 0, (int32_t)v, deg, rs);
+        farq.push(to_far, (int32_t)v, 0);
+    }
+    return nimp;
+}
+
 __device__ __forceinline__ long long sssp_gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
 
+template <bool kPacked>
 __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
+    using RelaxOp = RelaxOpT<kPacked>;
+    const int32_t *Cs = kPacked ? reinterpret_cast<const int32_t *>(a.CW) : a.C;  // the advance's edge stream
     const bool env_stream = a.stream_queues;
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -224,14 +317,29 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             farq.counter = &a.ctl->far_count[fp];
             RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep, policy_evict_first()};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.qr[k & 1], f, mf};
+            const bool pull = a.CWt && (a.direction == 2 || (a.direction == 0 && (double)mf * a.alpha > (double)a.m));
+            if (pull && tid == 0 && k < kMaxStatRecords) a.stats[k].direction = 5;  // pull relax
+            if (pull) {
+                // frontier queue -> bitmap, then every vertex pulls over its in-edges
+                const int64_t nwords = (a.n + 31) / 32;
+                for (int64_t w = tid; w < nwords; w += nthreads) a.fb[w] = 0u;
+                grid.sync();
+                const int32_t *qc = a.qv[k & 1];
+                for (int64_t j = tid; j < f; j += nthreads) {
+                    const int32_t v = qc[j];
+                    atomicOr(a.fb + (v >> 5), 1u << (v & 31));
+                }
+                grid.sync();
+                op.nimp = sssp_pull_step(a, thr, 2 * it, gw, nw, nearq, farq, pol_keep);
+            } else
             // same auto rule as BFS (reading A-4): short lists -> thread/warp/CTA
             if (f < a.lb_threshold && mf <= 16 * f && (int64_t)s->ctl[5] <= kTwcMaxDeg)  // no long list (see bfs.cu)
-                expand_twc(fr, a.C, op, &s->win);
+                expand_twc(fr, Cs, op, &s->win);
             else
 #if GR_SSSP_PIPE
                 expand_pipe<kSsspStages, true>(fr, a.C, a.W, gw, nw, op, &s->pipe[wib]);
 #else
-                expand_lb(fr, a.C, gw, nw, op, &a.ctl->slot[k & 3].work, 4);
+                expand_lb(fr, Cs, gw, nw, op, &a.ctl->slot[k & 3].work, 4);
 #endif
             nearq.finish_cta(s->wsum);
             farq.finish_cta(s->wsum);
@@ -317,10 +425,18 @@ __global__ void unpack_kernel(const unsigned long long *dp, int64_t n, uint32_t 
     }
 }
 
-gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta, int *launches) {
+gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta, int32_t direction,
+                   double alpha, int *launches) {
+    if (direction != 1 && !g->CWt) {  // weighted in-lists for pull steps, built on first use
+        gr_status st = build_pull_weights(g);
+        if (st != GR_OK) return st;
+    }
     SsspArgs a;
     a.n = g->n; a.m = g->m;
-    a.R = g->R; a.C = g->C; a.W = g->W;
+    a.R = g->R; a.C = g->C; a.W = g->W; a.CW = g->CW;
+    a.Rt = g->Rt; a.CWt = g->CWt; a.fb = g->fbuf[0];
+    a.direction = direction;
+    a.alpha = alpha > 0 ? alpha : 4.0;
     a.dp = g->dp; a.stamp = g->stamp;
     for (int i = 0; i < 2; ++i) {
         a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.qr[i] = g->qr[i]; a.far[i] = g->farq[i];
@@ -332,11 +448,14 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.lb_threshold = env_int("GR_SSSP_LB_THRESHOLD", 65536);
     a.stream_queues = (int)env_int("GR_SSSP_STREAMQ", 0);
     a.S = g->pack_shift;
-    static int per_sm = 0;
+    const bool packed = g->CW != nullptr;
+    const void *fn = packed ? (const void *)sssp_kernel<true> : (const void *)sssp_kernel<false>;
+    static int per_sm_v[2] = {0, 0};
+    int &per_sm = per_sm_v[packed ? 1 : 0];
     const size_t smem = sizeof(SsspSmem);
     if (per_sm == 0) {
-        GR_CUDA(cudaFuncSetAttribute(sssp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sssp_kernel, kBlock, smem));
+        GR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBlock, smem));
     }
     if (per_sm < 1) { set_error("sssp_kernel cannot be resident"); return GR_ERR_CUDA; }
     int64_t ctas = (int64_t)g->num_sms * per_sm;
@@ -344,7 +463,7 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     if (cap_ctas > 0 && cap_ctas < ctas) ctas = cap_ctas;
     dim3 grid((unsigned)ctas), block(kBlock);
     void *args[] = {&a};
-    GR_CUDA(cudaLaunchCooperativeKernel((void *)sssp_kernel, grid, block, args, smem, g->stream));
+    GR_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, g->stream));
     unpack_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->dp, g->n, dist, pred);
     GR_CUDA(cudaGetLastError());
     count_launch(2);

@@ -142,7 +142,7 @@ class PartitionedGraph:
             dist = torch.empty(self.n_local, dtype=torch.int32, device=dev)
         if pred is None and want_pred:
             pred = torch.empty(self.n_local, dtype=torch.int32, device=dev)
-        o = gr_sssp_opts(int(delta) & 0xFFFFFFFF, 0)
+        o = gr_sssp_opts(int(delta) & 0xFFFFFFFF, 0, 1, 0.0)
         dp, _ = _ptr(dist)
         pp, _ = _ptr(pred)
         _check(load().gr_sssp(self.handle, int(src), dp, pp, ctypes.byref(o)))

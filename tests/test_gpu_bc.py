@@ -25,17 +25,17 @@ def gr():
     return gr
 
 
-def _check(gr, g, srcs, symmetric=True, host=False):
+def _check(gr, g, srcs, symmetric=True, host=False, direction="auto"):
     R, C, _ = g.numpy()
     G = gr.Graph(g.R.cuda(), g.C.cuda(), None, symmetric=symmetric)
     if host:
         out = torch.empty(g.n, dtype=torch.float64, pin_memory=True)
         sig = np.empty(g.n, np.float64)
-        G.bc(srcs, bc=out, sigma=sig)
+        G.bc(srcs, bc=out, sigma=sig, direction=direction)
         bc = out.numpy()
     else:
         sig_t = torch.empty(g.n, dtype=torch.float64, device="cuda")
-        bc = G.bc(srcs, sigma=sig_t).cpu().numpy()
+        bc = G.bc(srcs, sigma=sig_t, direction=direction).cpu().numpy()
         sig = sig_t.cpu().numpy()
     ref = oracle.bc(R, C, srcs)
     scale = max(1.0, float(np.abs(ref).max()))
@@ -91,3 +91,31 @@ def test_bc_edge_cases(gr):
     with pytest.raises(gr.GrError):
         G.bc([10])
     G.close()
+
+
+@pytest.mark.parametrize("direction", ["push", "pull", "auto"])
+def test_bc_pull_direction(gr, direction):
+    """Pull (bottom-up) forward levels (P:832-834 names BC as a next user of
+    pull; reading A-24): every level pulled, every level pushed, and the
+    auto rule give the oracle's values on skewed, directed, mesh and
+    multi-component graphs (hub in-lists > 32 edges take the warp path)."""
+    for g, sym in ((gg.kronecker(13, 16, seed=3), True), (gg.rmat(12, 8, seed=4), True),
+                   (gg.directed_random(3000, 20000, seed=5), False), (gg.grid(30, 40), True),
+                   (gg.from_edges(50, [(i, i + 1) for i in range(20)] + [(30, 31), (31, 32)]), True)):
+        srcs = gg.sources(g, 3)
+        _check(gr, g, srcs, symmetric=sym, direction=direction)
+
+
+def test_bc_pull_stats(gr):
+    """The auto rule pulls the dense middle level of a Kronecker graph and
+    reports each level's direction (gr_get_run_stats after gr_bc)."""
+    g = gg.kronecker(15, 16, seed=6)
+    G = gr.Graph(g.R.cuda(), g.C.cuda(), None, symmetric=True)
+    s = gg.sources(g, 1)[0]
+    G.bc([s], direction="auto")
+    st = G.run_stats()
+    dirs = [r["direction"] for r in st["levels"]]
+    assert dirs[0] == 1 and 2 in dirs
+    R, C, _ = g.numpy()
+    d, _ = oracle.bfs(R, C, s)
+    assert [r["frontier"] for r in st["levels"]] == [int((d == L).sum()) for L in range(len(dirs))]
