@@ -68,6 +68,10 @@ def parse():
     ap.add_argument("--prim", default="bfs", choices=["bfs", "sssp", "bc", "cc", "pr"])
     ap.add_argument("--direction", default="auto", choices=["auto", "push", "pull"])
     ap.add_argument("--delta", type=int, default=0)
+    ap.add_argument("--sssp-direction", default="auto", choices=["auto", "push", "pull"],
+                    help="SSSP near iterations: push, pull over in-edges, or the auto rule (A-24)")
+    ap.add_argument("--bc-direction", default="auto", choices=["auto", "push", "pull"],
+                    help="BC forward levels: push, pull, or the auto rule (A-24)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true")
@@ -446,7 +450,7 @@ def run_bc(args, rank, world, dev):
     bcv = torch.empty(n, dtype=torch.float64, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     for s in srcs[: args.warmup]:
-        G.bc([s], bc=bcv)
+        G.bc([s], bc=bcv, direction=args.bc_direction)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -457,7 +461,7 @@ def run_bc(args, rank, world, dev):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            G.bc([s], bc=bcv)
+            G.bc([s], bc=bcv, direction=args.bc_direction)
             e1.record()
             torch.cuda.synchronize()
             ms.append(e0.elapsed_time(e1))
@@ -503,12 +507,12 @@ def run_bc(args, rank, world, dev):
         out["clocks"] = clk.summary()
     # end to end: host (pinned) output buffer through the C ABI
     pin = torch.empty(n, dtype=torch.float64, pin_memory=True)
-    G.bc(mine[:1], bc=pin)
+    G.bc(mine[:1], bc=pin, direction=args.bc_direction)
     e2e_s = 0.0
     for s in mine:
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        G.bc([s], bc=pin)
+        G.bc([s], bc=pin, direction=args.bc_direction)
         e2e_s += time.perf_counter() - t0
     out["e2e"] = {"value": edges / e2e_s / 1e9, "unit": "GTEPS", "h2d_bytes_per_step": 4,
                   "d2h_bytes_per_step": 8 * n,
@@ -755,7 +759,7 @@ def main():
         if args.prim == "bfs":
             G.bfs(s, depth, pred, direction=direction, asynchronous=asynchronous)
         else:
-            G.sssp(s, depth, pred, delta=args.delta, asynchronous=asynchronous)
+            G.sssp(s, depth, pred, delta=args.delta, direction=args.sssp_direction, asynchronous=asynchronous)
 
     for s in warm_srcs:
         step(s)
@@ -863,7 +867,7 @@ def main():
         if args.prim == "bfs":
             G.bfs(s, pin_d, pin_p, direction=args.direction)
         else:
-            G.sssp(s, pin_d, pin_p, delta=args.delta)
+            G.sssp(s, pin_d, pin_p, delta=args.delta, direction=args.sssp_direction)
     e2e_edges, e2e_s, per_call = 0, 0.0, []
     for s in my_srcs:
         torch.cuda.synchronize()
@@ -871,7 +875,7 @@ def main():
         if args.prim == "bfs":
             G.bfs(s, pin_d, pin_p, direction=args.direction)
         else:
-            G.sssp(s, pin_d, pin_p, delta=args.delta)
+            G.sssp(s, pin_d, pin_p, delta=args.delta, direction=args.sssp_direction)
         per_call.append(time.perf_counter() - t0)
         e2e_s += per_call[-1]
         e2e_edges += G.run_stats()["reached_edges"]

@@ -168,7 +168,7 @@ typedef struct {
                             SSSP in P:832-834; reading A-24). Pull needs the packed
                             edge stream (gr_graph_info.packed_weights); otherwise
                             push runs. Partitioned graphs: push.               */
-    double alpha;        /* auto: pull when frontier edges * alpha > m; 0 = 4     */
+    double alpha;        /* auto: pull when frontier edges * alpha > m; 0 = 2     */
 } gr_sssp_opts;
 
 gr_status gr_sssp(gr_graph *g, int32_t src, uint32_t *dist_out, int32_t *pred_out,

@@ -34,6 +34,9 @@ constexpr int64_t kSmallE = 16384;  // small mode: max frontier edges
 #define GR_BFS_STAGES 0  // measured on C2 push: 2 and 4 stages are slower (smem displaces L1)
 #endif
 constexpr int kBfsStages = GR_BFS_STAGES;  // cp.async pipeline depth of the grid push advance (0: off)
+#ifndef GR_SPEC_R
+#define GR_SPEC_R 1  // small push steps load the targets' row offsets in parallel with the claims
+#endif
 constexpr int kSmallCntBits = 24;   // count field of the small-mode packed counter
 constexpr unsigned long long kSmallCntMask = (1ull << kSmallCntBits) - 1;
 
@@ -141,6 +144,15 @@ struct BfsPushOp {
                     : probe == 1 ? ld_probe(visited + (dst[u] >> 5), pol_keep)
                     : probe == 2 ? ld_l1(visited + (dst[u] >> 5)) : 0u;
         bool disc[U];
+        // small steps (no probe): the row offsets of every target are loaded
+        // speculatively, in parallel with the claims -- one dependent round trip
+        // less per level (high-diameter graphs run thousands of such levels)
+        int64_t spec[U];
+        const bool specr = GR_SPEC_R && probe == 0 && !idempotent && !claim_cas;
+        if (specr) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) spec[u] = ok[u] ? __ldg(R + dst[u]) : 0;
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t w = dst[u];
@@ -183,8 +195,8 @@ struct BfsPushOp {
                 depth[w] = next_depth;
                 if (pred) pred[w] = src[u];
                 if (fbn) atomicOr(fbn + (w >> 5), 1u << (w & 31));  // RED.OR
-                rs = R[w];
-                deg = R[w + 1] - rs;
+                rs = specr ? spec[u] : R[w];
+                deg = __ldg(R + w + 1) - rs;
                 ++ndisc;
             }
             app->push(disc[u] && deg > 0, w, deg, rs);

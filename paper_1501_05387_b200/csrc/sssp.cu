@@ -436,7 +436,7 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.R = g->R; a.C = g->C; a.W = g->W; a.CW = g->CW;
     a.Rt = g->Rt; a.CWt = g->CWt; a.fb = g->fbuf[0];
     a.direction = direction;
-    a.alpha = alpha > 0 ? alpha : 4.0;
+    a.alpha = alpha > 0 ? alpha : 2.0;  // measured on C3: pull pays only when m_f > m / 2
     a.dp = g->dp; a.stamp = g->stamp;
     for (int i = 0; i < 2; ++i) {
         a.qv[i] = g->qv[i]; a.qo[i] = g->qo[i]; a.qr[i] = g->qr[i]; a.far[i] = g->farq[i];

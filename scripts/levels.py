@@ -48,7 +48,7 @@ for s in SRCS:
             if a.prim == "bfs":
                 G.bfs(s, direction=d, idempotent=bool(a.idempotent))
             else:
-                G.sssp(s, delta=a.delta)
+                G.sssp(s, delta=a.delta, direction=os.environ.get("SSSP_DIR", "auto"))
         torch.cuda.synchronize()
         st = G.run_stats()
         tot = sum(r["ns"] for r in st["levels"])
