@@ -35,9 +35,11 @@ constexpr int64_t kSmallE = 16384;  // small mode: max frontier edges
 #endif
 constexpr int kBfsStages = GR_BFS_STAGES;  // cp.async pipeline depth of the grid push advance (0: off)
 #ifndef GR_SPEC_R
-#define GR_SPEC_R 1  // small push steps load the targets' row offsets in parallel with the claims
+#define GR_SPEC_R 0  // 1: small push steps load the targets' row offsets in parallel with the claims
+                     // (measured slower everywhere: C4 BFS 98.5 -> 106 ms, C2 0.144 -> 0.153 ms; spills)
 #endif
-constexpr int kSmallCntBits = 24;   // count field of the small-mode packed counter
+constexpr int kSmallCntBits = 24;
+constexpr int64_t kCtaFlushEdges = 16384;  // steps with at least this many frontier edges flush per CTA   // count field of the small-mode packed counter
 constexpr unsigned long long kSmallCntMask = (1ull << kSmallCntBits) - 1;
 
 struct BfsArgs {
@@ -666,7 +668,11 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             atomicMax(&s->bsum[3], tw);
 #endif
         }
-        app.finish_cta(s->wsum);  // its CTA barriers also complete the counters above
+        // wide steps: one queue atomic per CTA (finish_cta); narrow steps (a few
+        // warps hold entries): per-warp flushes, no extra CTA barriers (measured
+        // on C4: +1.1 us per level with finish_cta on its 512-4K-vertex levels)
+        if (mf >= kCtaFlushEdges) app.finish_cta(s->wsum);  // its CTA barriers also complete the counters
+        else { app.finish(); __syncthreads(); }
         GR_TSTAMP(6);
 #ifdef GR_TRACE
         if (g_bal && threadIdx.x == 0 && L < 64) {

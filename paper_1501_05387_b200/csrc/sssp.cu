@@ -341,8 +341,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
 #else
                 expand_lb(fr, Cs, gw, nw, op, &a.ctl->slot[k & 3].work, 4);
 #endif
-            nearq.finish_cta(s->wsum);
-            farq.finish_cta(s->wsum);
+            if (mf >= 16384) {  // wide step: one queue atomic per CTA (see bfs.cu kCtaFlushEdges)
+                nearq.finish_cta(s->wsum);
+                farq.finish_cta(s->wsum);
+            } else {
+                nearq.finish();
+                farq.finish();
+            }
             const unsigned long long ni = warp_sum<unsigned long long>(op.nimp);
             if (lane_id() == 0 && ni) atomicAdd(&s->bsum[0], ni);
             __syncthreads();
@@ -403,8 +408,13 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
                 nearq.push(to_near && deg > 0, v, deg, rs);
                 farq.push(to_far, v, 0);
             }
-            nearq.finish_cta(s->wsum);
-            farq.finish_cta(s->wsum);
+            if (fc >= 16384) {
+                nearq.finish_cta(s->wsum);
+                farq.finish_cta(s->wsum);
+            } else {
+                nearq.finish();
+                farq.finish();
+            }
             grid.sync();
             fp ^= 1;
         }
