@@ -45,12 +45,18 @@ def build(force=False, verbose=False, lib=None):
     deps = srcs + [os.path.join(CSRC, h) for h in HEADERS] + [__file__]
     if not force and not _stale(LIB, deps):
         return LIB
-    objs = []
-    logs = []
-    for s in srcs:
+    def compile_one(s):
         o = os.path.join(CSRC, os.path.basename(s) + ".o")
         cmd = [NVCC] + FLAGS + EXTRA + ["-c", s, "-o", o]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        return s, o, subprocess.run(cmd, capture_output=True, text=True)
+
+    # one nvcc per translation unit, in parallel (the units are independent)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    objs = []
+    logs = []
+    for s, o, r in results:
         logs.append(r.stderr)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
