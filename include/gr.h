@@ -107,6 +107,10 @@ typedef struct {
     int64_t device_bytes;    /* device memory currently owned by the graph      */
     int32_t packed_weights;  /* 1: SSSP streams the packed (C << 7) | W array
                                 (n < 2^25, weights <= 127; 4 B per edge)         */
+    int32_t bounded_degree;  /* 1: every out-degree <= 4 and n < 2^28: push and
+                                relax steps read a 16-B (BFS) / 32-B (SSSP, if
+                                weighted) per-vertex adjacency record instead of
+                                R + C (road-like graphs)           */
 } gr_graph_info;
 
 gr_status gr_graph_info_get(const gr_graph *g, gr_graph_info *out);

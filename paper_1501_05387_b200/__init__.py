@@ -56,7 +56,7 @@ class gr_graph_info(ctypes.Structure):
                 ("nonisolated", ctypes.c_int64), ("symmetric", ctypes.c_int32),
                 ("has_weights", ctypes.c_int32), ("max_weight", ctypes.c_uint32),
                 ("device", ctypes.c_int32), ("device_bytes", ctypes.c_int64),
-                ("packed_weights", ctypes.c_int32)]
+                ("packed_weights", ctypes.c_int32), ("bounded_degree", ctypes.c_int32)]
 
 
 class gr_level_stats(ctypes.Structure):

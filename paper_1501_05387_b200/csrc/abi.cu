@@ -73,6 +73,14 @@ using namespace gr;
 
 extern "C" {
 
+// debug only (not in gr.h): the raw overflow word of the last run (low byte =
+// which queue: 1 frontier/near, 2 far; bits 8.. = the slot count requested)
+unsigned long long gr_debug_overflow(gr_graph *h) {
+    unsigned long long v = 0;
+    cudaMemcpy(&v, &((Graph *)h)->ctl->overflow, sizeof(v), cudaMemcpyDeviceToHost);
+    return v;
+}
+
 const char *gr_last_error(void) { return g_err; }
 
 uint64_t gr_kernel_launch_count(void) { return g_launches.load(); }
@@ -117,6 +125,7 @@ gr_status gr_graph_info_get(const gr_graph *h, gr_graph_info *out) {
     out->symmetric = g->symmetric; out->has_weights = g->has_w; out->max_weight = g->max_w;
     out->device = g->device; out->device_bytes = g->bytes;
     out->packed_weights = g->CW != nullptr;
+    out->bounded_degree = g->ell != nullptr;
     return GR_OK;
 }
 

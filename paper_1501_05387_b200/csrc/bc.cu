@@ -79,23 +79,27 @@ struct BcFwdOp {
         int32_t d[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) d[u] = ok[u] ? __ldcg(&a->bv[dst[u]].depth) : -2;
+        // the claims of all U edges in flight, then the row offsets of the
+        // discovered ones in flight (each consumed inside its own branch was
+        // a dependent round trip apiece)
+        int32_t c[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) c[u] = d[u] == -1 ? atomicCAS(&a->bv[dst[u]].depth, -1, next) : d[u];
+        bool disc[U];
+        int64_t r0[U], r1[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int32_t w = dst[u];
-            bool disc = false;
-            int64_t deg = 0, rs = 0;
-            int32_t dw = d[u];
-            if (dw == -1) {
-                dw = atomicCAS(&a->bv[w].depth, -1, next);
-                disc = dw == -1;
-                if (disc) dw = next;
-            }
-            if (dw == next) atomicAdd(&a->bv[w].val, __longlong_as_double((long long)pay[u]));
-            if (disc) { rs = a->R[w]; deg = a->R[w + 1] - rs; }
+            disc[u] = d[u] == -1 && c[u] == -1;
+            const int32_t dw = disc[u] ? next : c[u];
+            if (dw == next) atomicAdd(&a->bv[dst[u]].val, __longlong_as_double((long long)pay[u]));  // RED
+            r0[u] = disc[u] ? a->R[dst[u]] : 0;
+            r1[u] = disc[u] ? a->R[dst[u] + 1] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
             // every discovered vertex joins its level's queue (degree 0 too:
             // the backward pass converts its sigma into coef)
-            app->push(disc, w, deg, rs);
-        }
+            app->push(disc[u], dst[u], r1[u] - r0[u], r0[u]);
     }
 };
 

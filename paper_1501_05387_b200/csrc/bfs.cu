@@ -49,6 +49,7 @@ struct BfsArgs {
     const int64_t *Rt;   // in-edges for pull (== R when symmetric)
     const int32_t *Ct;
     const int2 *ph;      // pull head {first in-neighbour, in-degree} per vertex (null: none)
+    const int4 *ell;     // bounded-degree adjacency (null: none; Graph::ell)
     uint32_t *visited;
     const uint32_t *noin;  // vertices with in-degree 0
     uint32_t *fbuf[3];     // rotating frontier bitmaps
@@ -74,6 +75,7 @@ struct BfsArgs {
     int32_t lb_chunks;         // dynamic merge-path pieces per warp (0: static partition)
     int32_t claim_cas;         // push claim: CAS on depth[] (1) or atomicOr on the bitmap (0)
     int64_t probe_skip_pct;    // push steps skip the culling probe while m_u >= this % of m
+    int32_t lazy_r;            // grid push: row offsets of discovered vertices loaded at the flush
 };
 
 template <int kNW>
@@ -155,38 +157,54 @@ struct BfsPushOp {
 #pragma unroll
             for (int u = 0; u < U; ++u) spec[u] = ok[u] ? __ldg(R + dst[u]) : 0;
         }
+        // candidates first, then every claim of the lane in flight before any
+        // result is read (a claim consumed inside its own branch made the U
+        // atomics of a lane one dependent round trip each: measured ~0.45 us
+        // apiece on B200, the largest term of a narrow level)
+        bool cand[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t w = dst[u];
             const uint32_t bit = 1u << (w & 31);
-            disc[u] = false;
-            bool cand = ok[u] && !(word[u] & bit);
+            cand[u] = ok[u] && !(word[u] & bit);
             // snapshot: the first warp of this CTA to reach w sets its bit in
             // shared memory; the CTA's later visitors of w stop here (culling
             // inside the CTA is exact; the global claim below stays the truth)
-            if (cand && w < sbits) cand = !(atom_or_shared(sbm + 4u * (uint32_t)(w >> 5), bit) & bit);
+            if (cand[u] && w < sbits) cand[u] = !(atom_or_shared(sbm + 4u * (uint32_t)(w >> 5), bit) & bit);
             if (idempotent) {
                 // warp-level culling heuristic (A-5 i): lanes of one warp that
                 // target the same vertex keep only the lowest lane
-                const unsigned peers = __match_any_sync(0xffffffffu, cand ? w : -1 - (int)lane_id());
-                cand = cand && (__ffs(peers) - 1 == (int)lane_id());
+                const unsigned peers = __match_any_sync(0xffffffffu, cand[u] ? w : -1 - (int)lane_id());
+                cand[u] = cand[u] && (__ffs(peers) - 1 == (int)lane_id());
             }
-            if (cand) {
-                if (idempotent) {
-                    if (*(volatile int32_t *)(depth + w) < 0) {
-                        disc[u] = true;
-                        atomicOr(visited + (w >> 5), bit);  // result unused -> RED.OR
-                    }
-                } else if (claim_cas) {
-                    // exactly-once per VERTEX: contention only between claims of
-                    // the same vertex, not of the 32 vertices sharing a bitmap word
-                    disc[u] = atomicCAS(depth + w, -1, next_depth) == -1;
-                    if (disc[u]) atomicOr(visited + (w >> 5), bit);  // RED.OR
-                } else {
-                    const uint32_t old = atomicOr(visited + (w >> 5), bit);
-                    disc[u] = !(old & bit);
-                }
+        }
+        if (idempotent) {
+            int32_t dv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) dv[u] = cand[u] ? *(volatile int32_t *)(depth + dst[u]) : 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                disc[u] = cand[u] && dv[u] < 0;
+                if (disc[u]) atomicOr(visited + (dst[u] >> 5), 1u << (dst[u] & 31));  // result unused -> RED.OR
             }
+        } else if (claim_cas) {
+            // exactly-once per VERTEX: contention only between claims of
+            // the same vertex, not of the 32 vertices sharing a bitmap word
+            int32_t r[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) r[u] = cand[u] ? atomicCAS(depth + dst[u], -1, next_depth) : 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                disc[u] = cand[u] && r[u] == -1;
+                if (disc[u]) atomicOr(visited + (dst[u] >> 5), 1u << (dst[u] & 31));  // RED.OR
+            }
+        } else {
+            uint32_t old[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                old[u] = cand[u] ? atomicOr(visited + (dst[u] >> 5), 1u << (dst[u] & 31)) : 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < U; ++u) disc[u] = !((old[u] >> (dst[u] & 31)) & 1u);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -197,11 +215,93 @@ struct BfsPushOp {
                 depth[w] = next_depth;
                 if (pred) pred[w] = src[u];
                 if (fbn) atomicOr(fbn + (w >> 5), 1u << (w & 31));  // RED.OR
-                rs = specr ? spec[u] : R[w];
-                deg = __ldg(R + w + 1) - rs;
+                if (!app->Rl) {
+                    rs = specr ? spec[u] : R[w];
+                    deg = __ldg(R + w + 1) - rs;
+                }
                 ++ndisc;
             }
-            app->push(disc[u] && deg > 0, w, deg, rs);
+            // lazy appender: the row offsets of the staged vertices are loaded
+            // at the flush, all at once (no dependent load per group here)
+            app->push(disc[u] && (app->Rl || deg > 0), w, deg, rs);
+        }
+    }
+};
+
+// Grid push step over the bounded-degree adjacency (expand_ell): the same
+// cond/claim/apply/filter as BfsPushOp, but each slot
+// carries the neighbour's out-degree, so a discovered vertex is appended
+// without loading R; its own ELL record is prefetched into L2 for the next
+// level (high-diameter graphs: one dependent DRAM round trip less per level).
+struct BfsEllOp {
+    uint32_t *visited;
+    uint32_t *fbn;       // next frontier bitmap (null: not maintained this level)
+    int32_t *depth;
+    int32_t *pred;
+    const int4 *ell;
+    int32_t next_depth;
+    int32_t idempotent;
+    Appender *app;
+    unsigned long long ndisc;
+    unsigned long long pol_keep;
+    int probe;           // as BfsPushOp::probe
+
+    __device__ __forceinline__ void slots(bool, int32_t v, int4 s4) {
+        const int32_t sl[4] = {s4.x, s4.y, s4.z, s4.w};
+        uint32_t word[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t w = sl[k] >> 3;
+            word[k] = sl[k] < 0 ? 0xffffffffu
+                    : probe == 1 ? ld_probe(visited + (w >> 5), pol_keep)
+                    : probe == 2 ? ld_l1(visited + (w >> 5)) : 0u;
+        }
+        bool disc[4], cand[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t w = sl[k] >> 3;
+            cand[k] = sl[k] >= 0 && !(word[k] & (1u << (w & 31)));
+        }
+        if (idempotent) {
+            int32_t dv[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t w = sl[k] >> 3;
+                const unsigned peers = __match_any_sync(0xffffffffu, cand[k] ? w : -1 - (int)lane_id());
+                cand[k] = cand[k] && (__ffs(peers) - 1 == (int)lane_id());
+                dv[k] = cand[k] ? *(volatile int32_t *)(depth + w) : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t w = sl[k] >> 3;
+                disc[k] = cand[k] && dv[k] < 0;
+                if (disc[k]) atomicOr(visited + (w >> 5), 1u << (w & 31));  // RED.OR
+            }
+        } else {
+            // all claims of the lane in flight before any result is read
+            uint32_t old[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int32_t w = sl[k] >> 3;
+                old[k] = cand[k] ? atomicOr(visited + (w >> 5), 1u << (w & 31)) : 0xffffffffu;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) disc[k] = !((old[k] >> ((sl[k] >> 3) & 31)) & 1u);
+        }
+        GR_TDEP(3, disc[0] + 2 * disc[1] + 4 * disc[2] + 8 * disc[3]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!__any_sync(0xffffffffu, disc[k])) continue;
+            const int32_t w = sl[k] >> 3;
+            const int32_t deg = sl[k] & 7;
+            if (disc[k]) {
+                depth[w] = next_depth;
+                if (pred) pred[w] = v;
+                if (fbn) atomicOr(fbn + (w >> 5), 1u << (w & 31));  // RED.OR
+                if (deg) asm volatile("prefetch.global.L2 [%0];" ::"l"(ell + w));
+                ++ndisc;
+            }
+            app->push(disc[k] && deg > 0, w, deg, 0);
         }
     }
 };
@@ -212,7 +312,8 @@ struct BfsPushOp {
 // queue of the next level and prefetch the head of its neighbour list into L2
 // (the next level reads it a few microseconds later). Entries beyond kSmallF
 // spill to the global queue, which then ends small mode.
-struct SmallPushOp {
+template <bool kEll>
+struct SmallPushOpT {
     uint32_t *visited;
     int32_t *depth;
     int32_t *pred;
@@ -227,6 +328,7 @@ struct SmallPushOp {
     int64_t *go_next;
     int64_t *gr_next;
     unsigned long long ndisc;
+    const int4 *ell;             // bounded-degree adjacency (slots(); null: edges())
 
     __device__ __forceinline__ unsigned long long entry(int32_t) { return 0ull; }
 
@@ -241,6 +343,30 @@ struct SmallPushOp {
             rs[u] = ok[u] ? R[dst[u]] : 0;
             re[u] = ok[u] ? R[dst[u] + 1] : 0;
         }
+        append<U>(old, rs, re, dst, src);
+    }
+
+    // bounded-degree adjacency (expand_ell): the degree rides in the slot, the
+    // discovered vertex's ELL record is what the next level loads
+    __device__ __forceinline__ void slots(bool, int32_t v, int4 s4) {
+        const int32_t sl[4] = {s4.x, s4.y, s4.z, s4.w};
+        uint32_t old[4];
+        int64_t rs[4], re[4];
+        int32_t dst[4], src[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            dst[k] = sl[k] >> 3;
+            src[k] = v;
+            rs[k] = 0;
+            re[k] = sl[k] & 7;
+            old[k] = sl[k] >= 0 ? atomicOr(visited + (dst[k] >> 5), 1u << (dst[k] & 31)) : 0xffffffffu;
+        }
+        append<4>(old, rs, re, dst, src);
+    }
+
+    template <int U>
+    __device__ __forceinline__ void append(const uint32_t *old, const int64_t *rs, const int64_t *re,
+                                           const int32_t *dst, const int32_t *src) {
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t w = dst[u];
@@ -271,8 +397,12 @@ struct SmallPushOp {
                     gr_next[pos] = rs[u];
                 }
                 if (deg > 0) {
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs[u]));
-                    if (deg > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs[u] + 32));
+                    if constexpr (kEll) {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(ell + w));
+                    } else {
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs[u]));
+                        if (deg > 32) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + rs[u] + 32));
+                    }
                 }
                 ++ndisc;
             }
@@ -311,7 +441,10 @@ __host__ __device__ constexpr size_t bfs_sbm_offset() { return (sizeof(BfsSmemT<
 // kPush: direction forced to push (gr_bfs_opts.direction = 1): the pull and
 // bitmap-conversion paths are compiled out, which frees registers for the
 // push advance (fewer spills at the 64-register cap).
-template <int kBlk, int kMinB, bool kPush = false>
+// kEll: the graph has the bounded-degree adjacency (Graph::ell); its push
+// steps use expand_ell (a separate instantiation: the general kernel keeps
+// its register allocation)
+template <int kBlk, int kMinB, bool kPush = false, bool kEll = false>
 __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
     constexpr int kNW = kBlk / kWarp;
     using BfsSmem = BfsSmemT<kNW>;
@@ -411,7 +544,9 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
         if (tid == 0 && L > st.closed && L - 1 < kMaxStatRecords) {
             gr_level_stats &sr = a.stats[L - 1];
             sr.discovered = (int64_t)s->ctl[1];
-            if (sr.direction == 2) sr.inspected_edges = (int64_t)s->ctl[2];
+            // the level's direction is in a register: reading sr.direction back
+            // was a dependent global load on CTA 0's critical path every level
+            if (st.prev_dir == 2) sr.inspected_edges = (int64_t)s->ctl[2];
             const long long t = gtimer();
             sr.ns = t - t_prev;
             t_prev = t;
@@ -428,6 +563,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             conv.counter = &cs.fpack;
             conv.dmax = nullptr;
             conv.cnt = 0;
+            conv.Rl = nullptr;
             bitmap_to_queue(a, a.fbuf[L % 3], gw, nw, conv);
             grid.sync();
             st.q_valid = 1;
@@ -471,12 +607,13 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
                             sr.discovered = 0; sr.inspected_edges = E; sr.aux = st.u_cnt; sr.ns = 0;
                         }
                     }
-                    SmallPushOp op{a.visited, a.depth, a.pred, a.R, a.C, Lc + 1, s->u.small.q[c ^ 1],
+                    SmallPushOpT<kEll> op{a.visited, a.depth, a.pred, a.R, a.C, Lc + 1, s->u.small.q[c ^ 1],
                                    s->u.small.rs[c ^ 1], s->u.small.off[c ^ 1], &s->pk[r1],
-                                   a.qv[(Lc + 1) & 1], a.qo[(Lc + 1) & 1], a.qr[(Lc + 1) & 1], 0ull};
+                                   a.qv[(Lc + 1) & 1], a.qo[(Lc + 1) & 1], a.qr[(Lc + 1) & 1], 0ull, a.ell};
                     SmemFrontier fr{s->u.small.q[c], s->u.small.off[c], s->u.small.rs[c], cf, E};
                     GR_TSTAMP(9);
-                    expand_lb(fr, a.C, (int64_t)wib, (int64_t)kNW, op);
+                    if constexpr (kEll) expand_ell(s->u.small.q[c], cf, a.ell, (int64_t)wib, (int64_t)kNW, op);
+                    else expand_lb(fr, a.C, (int64_t)wib, (int64_t)kNW, op);
                     GR_TSTAMP(5);
                     const unsigned long long ndw = warp_sum<unsigned long long>(op.ndisc);
                     if (lane_id() == 0 && ndw) atomicAdd(&s->nd[r1], ndw);
@@ -532,8 +669,13 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             }
             grid.sync();
             if (threadIdx.x == 0) {
-                const volatile long long *bs = a.ctl->bstate;
-                for (int k = 0; k < 7; ++k) s->ctl[k] = (unsigned long long)bs[k];
+                // independent L2 loads issued back to back (volatile loads were
+                // serialised: 7 round trips while the CTA waits at the barrier)
+                long long x[7];
+#pragma unroll
+                for (int k = 0; k < 7; ++k) x[k] = __ldcg(a.ctl->bstate + k);
+#pragma unroll
+                for (int k = 0; k < 7; ++k) s->ctl[k] = (unsigned long long)x[k];
             }
             __syncthreads();
             st.L = (int)(long long)s->ctl[0];
@@ -574,6 +716,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
         app.qr = a.qr[(L + 1) & 1];
         app.counter = &nxt.qpack;
         app.dmax = &nxt.dmax;
+        app.Rl = (!kEll && a.lazy_r) ? a.R : nullptr;
         uint32_t *fb_c = a.fbuf[L % 3];
         uint32_t *fb_n = a.fbuf[(L + 1) % 3];
         uint32_t *fb_z = a.fbuf[(L + 2) % 3];
@@ -603,7 +746,15 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             snapshot_bits(sbm_p, dir == 1 ? a.visited : fb_c, a.sbm_words);
             __syncthreads();
         }
-        if (dir == 1) {
+        if (kEll && dir == 1) {
+            BfsEllOp op{a.visited, st.fbn_clean ? fb_n : nullptr, a.depth, a.pred, a.ell, L + 1, a.idempotent,
+                        &app, 0ull, pol_keep,
+                        (mf < (1 << 16) || st.m_u * 100 >= a.m * a.probe_skip_pct) ? 0 : (st.m_u * 4 >= a.m ? 1 : 2)};
+            // warps interleaved over the CTAs: a narrow frontier uses every SM
+            expand_ell(a.qv[L & 1], f, a.ell, (int64_t)wib * gridDim.x + blockIdx.x, nw, op);
+            ndisc = op.ndisc;
+            st.fb_valid = st.fbn_clean;
+        } else if (dir == 1) {
             BfsPushOp op{a.visited, st.fbn_clean ? fb_n : nullptr, a.depth, a.pred, a.R, L + 1,
                          a.idempotent, &app, 0ull, pol_keep,
                          // probe: none for small steps and when most edges still lead to
@@ -706,6 +857,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     BfsArgs a;
     a.n = g->n; a.m = g->m;
     a.R = g->R; a.C = g->C; a.Rt = g->Rt; a.Ct = g->Ct; a.ph = g->ph;
+    a.ell = g->ell;
     a.visited = g->visited;
     a.noin = g->noin;
     for (int i = 0; i < 3; ++i) a.fbuf[i] = g->fbuf[i];
@@ -727,6 +879,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.lb_chunks = (int32_t)env_int("GR_LB_CHUNKS", 4);
     a.claim_cas = (int32_t)env_int("GR_CLAIM_CAS", 0);
     a.probe_skip_pct = env_int("GR_PROBE_SKIP_PCT", 75);
+    a.lazy_r = (int32_t)env_int("GR_LAZY_R", 1);
     if (a.small_f > kSmallF) a.small_f = kSmallF;
 
     // Kernel variant: graphs whose bitmap no
@@ -738,6 +891,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     if (optin == 0) GR_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, g->device));
     const bool push_only = a.direction == 1 && !use_snap && env_int("GR_PUSH_KERNEL", 0) != 0;  // measured 3% slower: off
     const void *fn = use_snap ? (const void *)bfs_kernel<1024, 1>
+                   : g->ell ? (const void *)bfs_kernel<kBlock, kMinBlocks, false, true>
                    : push_only ? (const void *)bfs_kernel<kBlock, kMinBlocks, true>
                                : (const void *)bfs_kernel<kBlock, kMinBlocks>;
     const int block = use_snap ? 1024 : kBlock;
@@ -753,8 +907,8 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     } else {
         smem = sizeof(BfsSmemT<kBlock / kWarp>);
     }
-    static bool attr_set[3] = {false, false, false};
-    const int variant = use_snap ? 1 : push_only ? 2 : 0;
+    static bool attr_set[4] = {false, false, false, false};
+    const int variant = use_snap ? 1 : g->ell ? 3 : push_only ? 2 : 0;
     if (!attr_set[variant]) {
         GR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - 1024));
         attr_set[variant] = true;

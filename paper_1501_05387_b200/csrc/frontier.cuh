@@ -40,8 +40,22 @@ static __device__ long long *g_bal;   // [64 levels][grid][2]: first / last warp
             g_trace[g_trace_L * 16 + (k)] = t_;                                             \
         }                                                                                   \
     } while (0)
+// stamp k once the value x has ARRIVED (a load's result, not its issue):
+// the volatile local store waits for x, the memory-clobbering timer read
+// stays behind it
+#define GR_TDEP(k, val)                                                                      \
+    do {                                                                                    \
+        if (g_trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_L < 256) {            \
+            volatile int d_ = (int)(val);                                                   \
+            (void)d_;                                                                       \
+            long long t_;                                                                   \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)::"memory");                \
+            g_trace[g_trace_L * 16 + (k)] = t_;                                             \
+        }                                                                                   \
+    } while (0)
 #else
 #define GR_TSTAMP(k) do {} while (0)
+#define GR_TDEP(k, val) do {} while (0)
 #endif
 
 // ---------------------------------------------------------------------------
@@ -68,9 +82,48 @@ struct AppenderT {
     unsigned long long *overflow;
     unsigned long long *dmax = nullptr;  // max appended degree (offsets mode; null: not tracked)
     bool stream = false;            // streaming (evict-first) queue stores: keep L2 for per-vertex state
+    unsigned tag = 1;               // overflow code: which queue (diagnostics; any non-zero = overflow)
+    const int64_t *Rl = nullptr;    // lazy row offsets (offsets mode): push() stages the vertex only and
+                                    // the flush loads R[v], R[v+1] of all staged entries at once, so a
+                                    // discovery costs no dependent load inside the edge loop
+
+    // Lazy mode: row start and degree of every staged entry, loaded together
+    // (one round trip per flush instead of one per discovering edge group);
+    // entries of out-degree 0 are dropped (a frontier holds vertices with
+    // edges to expand). Returns the new count.
+    __device__ __forceinline__ int fill_from_R(int k) {
+        const unsigned l = lane_id();
+        constexpr int kR = kCap / 32;
+        int32_t v[kR];
+        int64_t r0[kR], r1[kR];
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            const int j = r * 32 + (int)l;
+            v[r] = (j < k) ? sv[j] : -1;
+            r0[r] = (v[r] >= 0) ? Rl[v[r]] : 0;
+            r1[r] = (v[r] >= 0) ? Rl[v[r] + 1] : 0;
+        }
+        __syncwarp();
+        int out = 0;
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+            const bool keep = r1[r] > r0[r];
+            const unsigned bm = __ballot_sync(0xffffffffu, keep);
+            if (keep) {
+                const int pos = out + __popc(bm & lanemask_lt());
+                sv[pos] = v[r];
+                sd[pos] = (int32_t)(r1[r] - r0[r]);
+                sr[pos] = r0[r];
+            }
+            out += __popc(bm);
+        }
+        __syncwarp();
+        return out;
+    }
 
     __device__ __forceinline__ void flush() {
         const unsigned l = lane_id();
+        if (Rl) cnt = fill_from_R(cnt);
         const int k = cnt;
         constexpr int kR = kCap / 32;
         // pass 1: total degree (and max) of the staged entries
@@ -97,7 +150,7 @@ struct AppenderT {
         base = __shfl_sync(0xffffffffu, base, 0);
         const unsigned long long cbase = qo ? (base & ((1ull << S) - 1)) : base;
         if ((int64_t)(cbase + k) > cap) {
-            if (l == 0) atomicExch(overflow, 1ull);
+            if (l == 0) atomicExch(overflow, (unsigned long long)tag | ((cbase + k) << 8));
         } else {
             // pass 2: exclusive degree prefix of each entry, then the writes
             int64_t run = qo ? (int64_t)(base >> S) : 0;
@@ -129,12 +182,12 @@ struct AppenderT {
         cnt = 0;
     }
 
-    // v: vertex, d: its out-degree, rs: R[v] (offsets mode)
+    // v: vertex, d: its out-degree, rs: R[v] (offsets mode; ignored in lazy mode)
     __device__ __forceinline__ void push(bool has, int32_t v, int64_t d, int64_t rs = 0) {
         const unsigned mask = __ballot_sync(0xffffffffu, has);
         if (mask == 0) return;
         const int pos = cnt + __popc(mask & lanemask_lt());
-        if (has) { sv[pos] = v; if (qo) { sd[pos] = (int32_t)d; sr[pos] = rs; } }
+        if (has) { sv[pos] = v; if (qo && !Rl) { sd[pos] = (int32_t)d; sr[pos] = rs; } }
         cnt += __popc(mask);
         __syncwarp();
         if (cnt > kCap - 32) flush();
@@ -156,6 +209,7 @@ struct AppenderT {
     __device__ __forceinline__ void finish_cta(unsigned long long *sw) {
         const unsigned l = lane_id();
         const int wi = threadIdx.x >> 5, nwb = blockDim.x >> 5;
+        if (Rl && cnt > 0) cnt = fill_from_R(cnt);
         const int k = cnt;
         constexpr int kR = kCap / 32;
         int64_t tot = 0;
@@ -192,7 +246,7 @@ struct AppenderT {
             const unsigned long long base = sw[2 * nwb] + sw[wi];
             const unsigned long long cbase = qo ? (base & ((1ull << S) - 1)) : base;
             if ((int64_t)(cbase + k) > cap) {
-                if (l == 0) atomicExch(overflow, 1ull);
+                if (l == 0) atomicExch(overflow, (unsigned long long)tag | ((cbase + k) << 8));
             } else {
                 int64_t run = qo ? (int64_t)(base >> S) : 0;
 #pragma unroll 4
@@ -320,6 +374,38 @@ __device__ __forceinline__ int64_t warp_lower_bound(int64_t F, int64_t t, Key ke
     return lo + __popc(__ballot_sync(0xffffffffu, less));
 }
 
+// Both ends of a merge-path piece at once: the two half-warps run 16-ary
+// searches side by side (one memory round trip per round for both), so a
+// piece costs ceil(log16 F) dependent rounds instead of 2 ceil(log32 F) --
+// e.g. 1 instead of 2 for a frontier of <= 16 hubs.
+template <class Key>
+__device__ __forceinline__ void warp_lower_bound2(int64_t F, int64_t t0, int64_t t1, Key key, int64_t &r0,
+                                                  int64_t &r1) {
+    const unsigned l = lane_id(), hl = l & 15;
+    const unsigned hmask = (l >> 4) ? 0xffff0000u : 0x0000ffffu;
+    const int64_t t = (l >> 4) ? t1 : t0;
+    int64_t lo = 0, hi = F;  // answer in [lo, hi]
+    for (;;) {
+        const bool big = hi - lo > 16;
+        if (!__any_sync(0xffffffffu, big)) break;
+        const int64_t step = (hi - lo) >> 4;
+        const int64_t p = lo + (int64_t)(hl + 1) * step - 1;
+        const bool less = big && key(p) < t;
+        const unsigned b = __ballot_sync(0xffffffffu, less) & hmask;
+        if (big) {
+            const int k = __popc(b);
+            const int64_t nlo = (k == 0) ? lo : lo + (int64_t)k * step;
+            const int64_t nhi = (k == 16) ? hi : lo + (int64_t)(k + 1) * step - 1;
+            lo = nlo; hi = nhi;
+        }
+    }
+    const int64_t p = lo + hl;
+    const bool less = p < hi && key(p) < t;
+    const int64_t res = lo + __popc(__ballot_sync(0xffffffffu, less) & hmask);
+    r0 = __shfl_sync(0xffffffffu, res, 0);
+    r1 = __shfl_sync(0xffffffffu, res, 16);
+}
+
 // ---------------------------------------------------------------------------
 // Frontier views: where the queue of the current level lives.
 //   GlobalFrontier: vertex ids, exclusive degree prefix and row starts R[v]
@@ -390,8 +476,16 @@ __device__ __forceinline__ void expand_lb_range(const Front &fr, const int32_t *
                                                 int64_t d1, Op &op) {
     const int64_t F = fr.F, E = fr.E;
     auto mkey = [&](int64_t i) { return fr.off(i) + i; };  // merged position of vertex i
+#ifndef GR_LB2
+#define GR_LB2 1
+#endif
+#if GR_LB2
+    int64_t i0, i1;
+    warp_lower_bound2(F, d0, d1, mkey, i0, i1);
+#else
     const int64_t i0 = warp_lower_bound(F, d0, mkey);
     const int64_t i1 = warp_lower_bound(F, d1, mkey);
+#endif
     GR_TSTAMP(1);
     const int64_t e0 = d0 - i0, e1 = d1 - i1;
     if (e0 >= e1) return;
@@ -665,6 +759,67 @@ __device__ __forceinline__ void expand_twc(const Front &fr, const int32_t *__res
             for (int u = 0; u < kUnroll; ++u) dst[u] = ok[u] ? ld_stream(C + eidx[u], pol) : 0;
             op.template edges<kUnroll>(ok, src, sp, dst, eidx);
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// RemoveRedundant stamp of SSSP ("a bitmap flag array associated
+// with the frontier", reading A-7): the key of iteration `base` = 2*it and
+// slice is base + 1 for the near queue, base for the far pile, claimed with
+// atomicMax. A far improvement that lands after a near one can then never
+// re-open the near slot, so a vertex enters the near queue at most once per
+// iteration (with atomicExch of alternating keys, the sequence near, far,
+// near admitted it twice -- measured: near queue > n on a dense graph).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int32_t stamp_key(int32_t base, bool far) { return base + (far ? 0 : 1); }
+
+// ---------------------------------------------------------------------------
+// Bounded-degree advance (Graph::ell, every out-degree <= 4): one frontier
+// vertex per lane, its whole neighbour list in one aligned 16-byte load --
+// the thread-granular class of P:693-706 with no prefix, search or row-offset
+// lookup. Frontier entry j goes to lane j%32 of warp (j/32) of the grid,
+// warps interleaved over the CTAs so a narrow frontier spreads over all SMs.
+// Op must provide slots(valid, v, int4 s) (warp-converged).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int4 ld_ell(const int4 *p) {
+    int4 r;
+    asm volatile("ld.global.nc.v4.s32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+    return r;
+}
+
+template <class Op>
+__device__ __forceinline__ void expand_ell(const int32_t *qv, int64_t f, const int4 *__restrict__ ell, int64_t gw,
+                                           int64_t nw, Op &op) {
+    const unsigned l = lane_id();
+    for (int64_t j0 = gw * 32; j0 < f; j0 += nw * 32) {
+        const int64_t j = j0 + l;
+        const bool valid = j < f;
+        const int32_t v = valid ? qv[j] : 0;
+        GR_TDEP(1, v);
+        const int4 s = valid ? ld_ell(ell + v) : make_int4(-1, -1, -1, -1);
+        GR_TDEP(2, s.x);
+        op.slots(valid, v, s);
+        GR_TSTAMP(4);
+    }
+}
+
+// Weighted variant (SSSP, Graph::ellw): the frontier vertex's payload
+// (op.entry, e.g. its distance) and its 32-byte record (ids, then
+// (weight << 3) | degree per slot) are loaded in parallel.
+// Op must provide entry(v) and slots(valid, v, pay, int4 ids, int4 wts).
+template <class Op>
+__device__ __forceinline__ void expand_ellw(const int32_t *qv, int64_t f, const int4 *__restrict__ ellw, int64_t gw,
+                                            int64_t nw, Op &op) {
+    const unsigned l = lane_id();
+    for (int64_t j0 = gw * 32; j0 < f; j0 += nw * 32) {
+        const int64_t j = j0 + l;
+        const bool valid = j < f;
+        const int32_t v = valid ? qv[j] : 0;
+        const unsigned long long pay = valid ? op.entry(v) : 0ull;
+        const int4 id = valid ? ld_ell(ellw + 2 * (int64_t)v) : make_int4(-1, -1, -1, -1);
+        const int4 wt = valid ? ld_ell(ellw + 2 * (int64_t)v + 1) : make_int4(0, 0, 0, 0);
+        op.slots(valid, v, pay, id, wt);
     }
 }
 

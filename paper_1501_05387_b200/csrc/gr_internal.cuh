@@ -121,6 +121,15 @@ struct Graph {
     int64_t *Rt = nullptr;        // CSC (== R when symmetric)
     int32_t *Ct = nullptr;
     int2 *ph = nullptr;           // pull head: {Ct[Rt[v]] or -1, in-degree} (pull steps, pull.cuh)
+    // Bounded-degree ("ELL") adjacency, built when every out-degree is <= 4
+    // (road-like graphs, C4): one 16-B record per vertex whose slot k holds
+    // (k-th neighbour w << 3) | out-degree(w), or -1. A push step reads a
+    // frontier vertex's whole list with one aligned load and learns each
+    // discovered vertex's degree without touching R (graph.cu, frontier.cuh).
+    int4 *ell = nullptr;
+    // SSSP companion: 32 B per vertex, ellw[2v] = the four neighbour ids (-1),
+    // ellw[2v+1] = (w(v, nbr) << 3) | out-degree(nbr) per slot.
+    int4 *ellw = nullptr;
 
     // per-run scratch (device)
     uint32_t *visited = nullptr;  // [nwords] visited bitmap (P:793-799 culling)

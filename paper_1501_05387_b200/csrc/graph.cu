@@ -27,7 +27,7 @@ void dev_free_all(Graph *g) {
                     g->qv[0], g->qv[1], g->qo[0], g->qo[1], g->qr[0], g->qr[1], g->depth_buf, g->pred_buf,
                     g->dist_buf, g->dp, g->stamp, g->farq[0], g->farq[1], g->ctl, g->stats_dev,
                     g->sent, g->ps_best, g->ps_sstamp, g->bc_vert, g->bc_sig, g->bc_delta, g->bc_buf, g->bc_cnt,
-                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph, g->ps_ship, g->CW, g->CWt};
+                    g->cc_ctl, g->cc_list[0], g->cc_list[1], g->pr_inv, g->pr_acc, g->pr_cnt, g->ph, g->ps_ship, g->CW, g->CWt, g->ell, g->ellw};
     for (void *p : ptrs)
         if (p) cudaFree(p);
     if (g->stats_host) cudaFreeHost(g->stats_host);
@@ -228,6 +228,34 @@ gr_status sort_lists_by_degree(Graph *g, cudaStream_t s, int blocks, const int32
 done:
     cudaFree(k0); cudaFree(k1); cudaFree(v0); cudaFree(v1); cudaFree(tbuf);
     return st;
+}
+
+// Bounded-degree adjacency (gr_internal.cuh Graph::ell / ellw): every
+// out-degree <= 4, ids < 2^28. Slot k of vertex v: (C[R[v]+k] << 3) | deg(C[R[v]+k]).
+__global__ void build_ell_kernel(const int64_t *R, const int32_t *C, const uint32_t *W, int64_t n,
+                                 int4 *ell, int4 *ellw) {
+    const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n; v += nt) {
+        const int64_t r0 = R[v];
+        const int d = (int)(R[v + 1] - r0);
+        int s[4], id[4], wt[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            s[k] = -1; id[k] = -1; wt[k] = 0;
+            if (k < d) {
+                const int32_t w = C[r0 + k];
+                const int dw = (int)(R[w + 1] - R[w]);
+                s[k] = (w << 3) | dw;
+                id[k] = w;
+                wt[k] = W ? (int)((W[r0 + k] << 3) | (uint32_t)dw) : 0;
+            }
+        }
+        ell[v] = make_int4(s[0], s[1], s[2], s[3]);
+        if (ellw) {
+            ellw[2 * v] = make_int4(id[0], id[1], id[2], id[3]);
+            ellw[2 * v + 1] = make_int4(wt[0], wt[1], wt[2], wt[3]);
+        }
+    }
 }
 
 // Packed SSSP edge stream: CW[e] = (C[e] << 7) | W[e] (sssp.cu RelaxOpT<true>).
@@ -450,6 +478,16 @@ gr_status graph_create(int64_t n, int64_t m, const int64_t *R, const int32_t *C,
     if (W && m > 0 && ncols < (1ll << 25) && g->max_w <= 127 && env_int("GR_PACK_W", 1)) {
         TRY(dev_alloc(g, (void **)&g->CW, m * sizeof(uint32_t) + 16));
         pack_cw_kernel<<<blocks, 256, 0, s>>>(g->C, g->W, m, g->CW);
+        count_launch();
+        TRYC(cudaGetLastError());
+    }
+    // Bounded-degree adjacency for high-diameter, low-degree graphs (C4): a
+    // push step then costs one aligned 16-B load per frontier vertex and no
+    // row-offset lookup per discovered vertex.
+    if (ncols == n && m > 0 && g->max_deg <= 4 && n < (1ll << 28) && env_int("GR_ELL", 1)) {
+        TRY(dev_alloc(g, (void **)&g->ell, n * sizeof(int4)));
+        if (W && g->max_w < (1u << 28)) TRY(dev_alloc(g, (void **)&g->ellw, 2 * n * sizeof(int4)));
+        build_ell_kernel<<<blocks, 256, 0, s>>>(g->R, g->C, W ? g->W : nullptr, n, g->ell, g->ellw);
         count_launch();
         TRYC(cudaGetLastError());
     }

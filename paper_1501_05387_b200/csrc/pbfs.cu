@@ -100,24 +100,30 @@ struct PPushOp {
     template <int U, class T5>
     __device__ __forceinline__ void edges(const bool *ok, const int32_t *src, const unsigned long long *,
                                           const int32_t *dst, const T5 *) {
-        bool disc[U], ship[U];
+        // probes of all U edges, then all claims in flight, then the results
+        // (an atomic consumed inside its own branch costs a round trip apiece)
+        bool disc[U], ship[U], own[U];
+        uint32_t word[U], *cw[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t w = dst[u];
             const int64_t lw = (int64_t)w - a->v_begin;
-            const bool owned = lw >= 0 && lw < a->n_local;
-            disc[u] = false;
-            ship[u] = false;
-            if (!ok[u]) continue;
-            if (owned) {
-                const uint32_t bit = 1u << (lw & 31);
-                const bool seen = probe && (ld_probe(a->visited + (lw >> 5), pol_keep) & bit);
-                if (!seen) disc[u] = !(atomicOr(a->visited + (lw >> 5), bit) & bit);
-            } else {
-                const uint32_t bit = 1u << (w & 31);
-                if (!(ld_probe(a->sent + (w >> 5), pol_keep) & bit))
-                    ship[u] = !(atomicOr(a->sent + (w >> 5), bit) & bit);
-            }
+            own[u] = lw >= 0 && lw < a->n_local;
+            cw[u] = own[u] ? a->visited + (lw >> 5) : a->sent + (w >> 5);  // claim word
+            word[u] = !ok[u] ? 0xffffffffu : (own[u] && !probe) ? 0u : ld_probe(cw[u], pol_keep);
+        }
+        uint32_t old[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t bit = 1u << ((own[u] ? (int32_t)((int64_t)dst[u] - a->v_begin) : dst[u]) & 31);
+            old[u] = !(word[u] & bit) ? atomicOr(cw[u], bit) : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t bit = 1u << ((own[u] ? (int32_t)((int64_t)dst[u] - a->v_begin) : dst[u]) & 31);
+            const bool got = !(old[u] & bit);
+            disc[u] = got && own[u];
+            ship[u] = got && !own[u];
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -125,16 +131,13 @@ struct PPushOp {
             const int32_t parent = (int32_t)(a->v_begin + src[u]);
             if (__any_sync(0xffffffffu, disc[u])) {
                 const int64_t lw = (int64_t)w - a->v_begin;
-                int64_t deg = 0, rs = 0;
                 if (disc[u]) {
                     a->depth[lw] = next_depth;
                     if (a->pred) a->pred[lw] = parent;
                     if (fbn) atomicOr(fbn + (lw >> 5), 1u << (lw & 31));  // RED.OR
-                    rs = a->R[lw];
-                    deg = a->R[lw + 1] - rs;
                     ++ndisc;
                 }
-                app->push(disc[u] && deg > 0, (int32_t)lw, deg, rs);
+                app->push(disc[u], (int32_t)lw, 0, 0);  // lazy appender: R loaded at the flush
             }
             const unsigned shm = __ballot_sync(0xffffffffu, ship[u]);
             if (shm) {
@@ -250,6 +253,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
     app.S = a.S;
     app.cap = 2 * a.n_local;
     app.overflow = &a.ctl->overflow;
+    app.Rl = a.R;  // lazy: every pushed id is local; its row offsets are loaded at the flush
     const unsigned long long pol_keep = policy_evict_last();
     const PullView view{a.n_local, a.R, a.R, a.Cp, a.ph, a.visited, a.depth, a.pred};
     const uint32_t *gfront_own[2] = {reinterpret_cast<const uint32_t *>(a.sym[a.rank] + A.off_gfront[0]),
@@ -332,6 +336,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
                 conv.counter = &a.ctl->slot[L & 3].fpack;
                 conv.dmax = nullptr;
                 conv.cnt = 0;
+                conv.Rl = nullptr;
                 bitmap_to_queue(view, fb_c, gw, nw, conv);
                 grid.sync();
                 q_valid = true;
@@ -366,13 +371,11 @@ __global__ void __launch_bounds__(kBlk, kMinB) pbfs_kernel(const __grid_constant
                                 a.depth[lw] = L + 1;
                                 if (a.pred) a.pred[lw] = pr.y;
                                 if (fbn_clean) atomicOr(fb_n + (lw >> 5), bit);  // RED.OR
-                                rs = a.R[lw];
-                                deg = a.R[lw + 1] - rs;
                                 ++ndisc;
                             }
                         }
                     }
-                    app.push(disc && deg > 0, (int32_t)lw, deg, rs);
+                    app.push(disc, (int32_t)lw, deg, rs);  // lazy appender: R at the flush
                 }
                 app.finish_cta(sm.wsum);
                 istart = iend;

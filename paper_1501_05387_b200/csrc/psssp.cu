@@ -85,8 +85,8 @@ __device__ __forceinline__ int sp_relax(const SRank &a, int64_t lv, unsigned lon
     const unsigned long long old = atomicMin(a.dp + lv, (nd << 32) | parent);
     if (nd >= (old >> 32)) return 0;
     const bool far = nd >= thr;
-    const int32_t key = key_near + (far ? 1 : 0);
-    if (atomicExch(a.stamp + lv, key) == key) return 0;
+    const int32_t key = stamp_key(key_near, far);
+    if (atomicMax(a.stamp + lv, key) >= key) return 0;
     return far ? 2 : 1;
 }
 
@@ -123,25 +123,41 @@ struct PSRelaxOp {
             const bool owned = lv >= 0 && lv < a->n_local;
             cur[u] = ok[u] ? ld_probe(owned ? a->dp + lv : a->best + vv[u], pol) : 0ull;
         }
+        // UpdateLabel (owned: dp, remote: best) of all U edges in flight, then
+        // the stamps of the improved ones in flight, then the filter -- each
+        // atomic consumed inside its own branch was a round trip apiece
+        unsigned long long old[U];
+        bool tr[U], own[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t lv = (int64_t)vv[u] - a->v_begin;
+            own[u] = lv >= 0 && lv < a->n_local;
+            const unsigned long long nd = du[u] + w[u];
+            const uint32_t parent = (uint32_t)(a->v_begin + src[u]);
+            tr[u] = ok[u] && nd < (cur[u] >> 32);
+            old[u] = tr[u] ? atomicMin(own[u] ? a->dp + lv : a->best + vv[u], (nd << 32) | parent) : 0ull;
+        }
+        int32_t ex[U], key[U];
+        bool imp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t lv = (int64_t)vv[u] - a->v_begin;
+            const unsigned long long nd = du[u] + w[u];
+            imp[u] = tr[u] && nd < (old[u] >> 32);
+            key[u] = own[u] ? stamp_key(key_near, nd >= thr) : step;
+            // owned: near/far stamp (atomicMax, stamp_key); remote: one shipment per step
+            ex[u] = !imp[u] ? key[u] : own[u] ? atomicMax(a->stamp + lv, key[u]) : atomicExch(a->sstamp + vv[u], key[u]);
+            if (imp[u] && own[u]) ++nimp;
+        }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int32_t v = vv[u];
             const int64_t lv = (int64_t)v - a->v_begin;
-            const bool owned = lv >= 0 && lv < a->n_local;
-            const unsigned long long nd = du[u] + w[u];
-            const uint32_t parent = (uint32_t)(a->v_begin + src[u]);
-            int kind = 0;
-            bool ship = false;
-            int64_t deg = 0, rs = 0;
-            if (ok[u] && owned) {
-                kind = sp_relax(*a, lv, nd, parent, thr, key_near, cur[u]);
-                if (kind) ++nimp;
-                if (kind == 1) { rs = a->R[lv]; deg = a->R[lv + 1] - rs; }
-            } else if (ok[u] && nd < (cur[u] >> 32)) {
-                const unsigned long long old = atomicMin(a->best + v, (nd << 32) | parent);
-                if (nd < (old >> 32)) ship = atomicExch(a->sstamp + v, step) != step;
-            }
-            nearq->push(kind == 1 && deg > 0, (int32_t)lv, deg, rs);
+            const bool first = imp[u] && (own[u] ? ex[u] < key[u] : ex[u] != key[u]);
+            const bool far = du[u] + w[u] >= thr;
+            const int kind = (first && own[u]) ? (far ? 2 : 1) : 0;
+            const bool ship = first && !own[u];
+            nearq->push(kind == 1, (int32_t)lv, 0, 0);  // lazy appender: R at the flush
             farq->push(kind == 2, (int32_t)lv, 0);
             const unsigned sm = __ballot_sync(0xffffffffu, ship);
             if (sm) {  // this step's ship list (one atomic per warp)
@@ -231,6 +247,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) psssp_kernel(const __grid_constan
     PsApp nearq, farq;
     nearq.sv = sm.sv[wib]; nearq.sd = sm.sd[wib]; nearq.sr = sm.sr[wib]; nearq.cnt = 0; nearq.S = a.S;
     nearq.cap = 2 * a.n_local;
+    nearq.Rl = a.R;  // lazy: every near id is local; row offsets loaded at the flush
     nearq.overflow = &a.ctl->overflow;
     farq.sv = sm.fv[wib]; farq.sd = nullptr; farq.sr = nullptr; farq.cnt = 0; farq.S = 0;
     farq.qo = nullptr; farq.qr = nullptr;
@@ -345,10 +362,10 @@ __global__ void __launch_bounds__(kBlk, kMinB) psssp_kernel(const __grid_constan
                             kind = sp_relax(a, lv, (unsigned long long)(uint32_t)t.y, (uint32_t)t.z, thr, 2 * it,
                                             ld_probe(a.dp + lv, pol));
                             if (kind) ++nimp;
-                            if (kind == 1) { rs0 = a.R[lv]; deg = a.R[lv + 1] - rs0; }
+
                         }
                     }
-                    nearq.push(kind == 1 && deg > 0, (int32_t)lv, deg, rs0);
+                    nearq.push(kind == 1, (int32_t)lv, deg, rs0);  // lazy: R at the flush
                     farq.push(kind == 2, (int32_t)lv, 0);
                 }
                 nearq.finish_cta(sm.wsum);
@@ -401,14 +418,14 @@ __global__ void __launch_bounds__(kBlk, kMinB) psssp_kernel(const __grid_constan
                     const unsigned long long d = ld_probe(a.dp + v, pol) >> 32;
                     if (d >= thr_old) {  // else stale: already expanded below thr_old
                         const bool nearb = d < thr;
-                        const int32_t key = 2 * it + (nearb ? 0 : 1);
-                        if (atomicExch(a.stamp + v, key) != key) {
-                            if (nearb) { to_near = true; rs0 = a.R[v]; deg = a.R[v + 1] - rs0; }
+                        const int32_t key = stamp_key(2 * it, !nearb);
+                        if (atomicMax(a.stamp + v, key) < key) {
+                            if (nearb) to_near = true;
                             else to_far = true;
                         }
                     }
                 }
-                nearq.push(to_near && deg > 0, v, deg, rs0);
+                nearq.push(to_near, v, deg, rs0);  // lazy: R at the flush
                 farq.push(to_far, v, 0);
             }
             nearq.finish_cta(sm.wsum);

@@ -58,10 +58,13 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
     const unsigned long long pol = policy_evict_first();
     const bool sym = a.Rt == a.R;
     const uint32_t tail = (a.n & 31) ? ((1u << (a.n & 31)) - 1u) : 0xffffffffu;
-    auto fbit = [&](int32_t u) -> bool {
-        const uint32_t fw = u < sbits ? lds_u32(sbm + 4u * (uint32_t)(u >> 5)) : __ldg(fcur + (u >> 5));
-        return (fw >> (u & 31)) & 1u;
+    // frontier word of u (u >= 0): loaded unconditionally by the callers and
+    // tested afterwards, so the probes of a lane are in flight together (a
+    // probe consumed inside a short-circuit branch costs a round trip each)
+    auto fword = [&](int32_t u) -> uint32_t {
+        return u < sbits ? lds_u32(sbm + 4u * (uint32_t)(u >> 5)) : __ldg(fcur + (u >> 5));
     };
+    auto fbit = [&](int32_t u) -> bool { return (fword(u) >> (u & 31)) & 1u; };
     int cnt = 0;  // warp-uniform
     auto process = [&](int k) {  // candidates wl[0, k), k <= 64
         int32_t v[2], par[2], u0[2];
@@ -75,18 +78,29 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
             // them (in-lists are ordered by neighbour degree, hubs first);
             // only unresolved lists read their row offset
             int2 h[2];
+            int64_t rt[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) h[q] = v[q] >= 0 ? __ldg(a.ph + v[q]) : make_int2(-1, 0);
+            // row offsets loaded speculatively with the heads (candidates are
+            // sorted: coalesced), so an unresolved list starts its scan one
+            // dependent round trip earlier
+#pragma unroll
+            for (int q = 0; q < 2; ++q) rt[q] = v[q] >= 0 ? __ldg(a.Rt + v[q]) : 0;
+            uint32_t fw[2];
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
                 u0[q] = h[q].x;
-                fnd[q] = u0[q] >= 0 && fbit(u0[q]);
+                fw[q] = u0[q] >= 0 ? fword(u0[q]) : 0u;
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+                fnd[q] = u0[q] >= 0 && ((fw[q] >> (u0[q] & 31)) & 1u);
                 par[q] = u0[q];
                 pc.insp += (u0[q] >= 0);
             }
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                beg[q] = (!fnd[q] && h[q].y > 1) ? a.Rt[v[q]] : 0;
+                beg[q] = (!fnd[q] && h[q].y > 1) ? rt[q] : 0;
                 end[q] = beg[q] + h[q].y;
             }
         } else {
@@ -97,9 +111,12 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
             }
 #pragma unroll
             for (int q = 0; q < 2; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Ct + beg[q], pol) : -1;
+            uint32_t fw[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) fw[q] = u0[q] >= 0 ? fword(u0[q]) : 0u;
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-                fnd[q] = u0[q] >= 0 && fbit(u0[q]);
+                fnd[q] = u0[q] >= 0 && ((fw[q] >> (u0[q] & 31)) & 1u);
                 par[q] = u0[q];
                 pc.insp += (u0[q] >= 0);
             }
@@ -116,13 +133,16 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
             const int64_t lim = (end[q] - nxt[q] > kPullLong) ? nxt[q] + kPullLong : end[q];
             for (int64_t e = nxt[q]; e < lim && !fnd[q]; e += 4) {
                 int32_t u[4];
+                uint32_t uw[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) u[j] = (e + j < lim) ? ld_stream(a.Ct + e + j, pol) : -1;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) uw[j] = u[j] >= 0 ? fword(u[j]) : 0u;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     if (!fnd[q] && u[j] >= 0) {
                         ++pc.insp;
-                        if (fbit(u[j])) { fnd[q] = true; par[q] = u[j]; }
+                        if ((uw[j] >> (u[j] & 31)) & 1u) { fnd[q] = true; par[q] = u[j]; }
                     }
                 }
             }

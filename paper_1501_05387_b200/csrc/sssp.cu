@@ -22,6 +22,8 @@ struct SsspArgs {
     const uint32_t *CW;       // packed (C << 7) | W, or null
     const int64_t *Rt;        // in-list offsets (== R when symmetric)
     const uint32_t *CWt;      // packed weighted in-lists (u << 7) | w(u,v), or null: no pull steps
+    const int4 *ellw;         // bounded-degree weighted adjacency (null: none; Graph::ellw)
+    int32_t lazy_r;           // near queue: row offsets loaded at the appender's flush
     uint32_t *fb;             // pull steps: bitmap of the near frontier [ceil(n/32)]
     int32_t direction;        // 0 auto, 1 push, 2 pull (near iterations; reading A-24)
     double alpha;             // auto: pull when m_f * alpha > m
@@ -76,7 +78,7 @@ struct RelaxOpT {
     const uint32_t *W;
     const int64_t *R;
     uint64_t thr;
-    int32_t key_near;   // 2*it   (A-7)
+    int32_t key_near;   // 2*it: stamp keys of this iteration (stamp_key, A-7)
     SsspAppender *nearq;
     SsspAppender *farq;
     unsigned long long nimp;
@@ -107,27 +109,81 @@ struct RelaxOpT {
             }
             cur[u] = ok[u] ? ld_probe(dp + vv[u], pol_keep) : 0ull;
         }
+        // UpdateLabel for every edge of the lane in flight at once, then the
+        // RemoveRedundant stamps of the improved ones at once (each atomic
+        // consumed inside its own branch made them one dependent round trip
+        // apiece), then the filter
+        unsigned long long old[U];
+        bool tr[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            bool to_near = false, to_far = false;
-            int64_t deg = 0, rs = 0;
-            const int32_t v = vv[u];
             const unsigned long long nd = du[u] + w[u];
-            if (ok[u] && nd < (cur[u] >> 32)) {
-                const unsigned long long pk = (nd << 32) | (unsigned int)src[u];
-                const unsigned long long old = atomicMin(dp + v, pk);
-                if (nd < (old >> 32)) {
-                    const bool far = nd >= thr;
-                    const int32_t key = key_near + (far ? 1 : 0);
-                    if (atomicExch(stamp + v, key) != key) {
-                        if (far) to_far = true;
-                        else { to_near = true; rs = R[v]; deg = R[v + 1] - rs; }
-                    }
-                    ++nimp;
-                }
-            }
-            nearq->push(to_near && deg > 0, v, deg, rs);
-            farq->push(to_far, v, 0);
+            tr[u] = ok[u] && nd < (cur[u] >> 32);
+            old[u] = tr[u] ? atomicMin(dp + vv[u], (nd << 32) | (unsigned int)src[u]) : 0ull;
+        }
+        bool imp[U];
+        int32_t ex[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long nd = du[u] + w[u];
+            imp[u] = tr[u] && nd < (old[u] >> 32);
+            const int32_t key = stamp_key(key_near, nd >= thr);
+            ex[u] = imp[u] ? atomicMax(stamp + vv[u], key) : key;
+            if (imp[u]) ++nimp;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const unsigned long long nd = du[u] + w[u];
+            const bool far = nd >= thr;
+            const bool first = imp[u] && ex[u] < stamp_key(key_near, far);
+            const bool to_near = first && !far;
+            int64_t deg = 0, rs = 0;
+            if (to_near && !nearq->Rl) { rs = R[vv[u]]; deg = R[vv[u] + 1] - rs; }
+            nearq->push(to_near && (nearq->Rl || deg > 0), vv[u], deg, rs);
+            farq->push(first && far, vv[u], 0);
+        }
+    }
+
+    // Bounded-degree adjacency (expand_ellw, Graph::ellw): the four (v, w)
+    // slots of frontier vertex u arrive in one 32-byte record whose weight
+    // words also carry deg(v). No culling probe: on these graphs a relax step
+    // is latency-bound, so the packed atomicMin is issued directly, with the
+    // pred field all ones: it lowers dp[v] only for a STRICTLY smaller
+    // distance (a tie leaves the current parent, as the probe-guarded push
+    // relax does; with zero weights a tie-won parent could close a pred
+    // cycle), and the winner then lowers the pred field to u with a
+    // fire-and-forget RED.MIN (same distance, any later smaller distance
+    // already beats both).
+    const int4 *ellw = nullptr;
+    __device__ __forceinline__ void slots(bool, int32_t u, unsigned long long du, int4 id4, int4 wt4) {
+        const int32_t id[4] = {id4.x, id4.y, id4.z, id4.w};
+        const int32_t wt[4] = {wt4.x, wt4.y, wt4.z, wt4.w};
+        unsigned long long nd[4], old[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            nd[k] = du + (unsigned long long)((uint32_t)wt[k] >> 3);
+            old[k] = id[k] >= 0 ? atomicMin(dp + id[k], (nd[k] << 32) | 0xffffffffull) : 0ull;
+        }
+        bool imp[4], far[4], first[4];
+        int32_t ex[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            imp[k] = id[k] >= 0 && nd[k] < (old[k] >> 32);
+            if (imp[k]) atomicMin(dp + id[k], (nd[k] << 32) | (unsigned int)u);  // result unused: RED.MIN
+            far[k] = nd[k] >= thr;
+            const int32_t key = stamp_key(key_near, far[k]);
+            ex[k] = imp[k] ? atomicMax(stamp + id[k], key) : key;  // all in flight, read below
+            if (imp[k]) ++nimp;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) first[k] = imp[k] && ex[k] < stamp_key(key_near, far[k]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t deg = wt[k] & 7;
+            const bool to_near = first[k] && !far[k];
+            if (to_near && deg) asm volatile("prefetch.global.L2 [%0];" ::"l"(ellw + 2 * (int64_t)id[k]));
+            nearq->push(to_near && deg > 0, id[k], deg, 0);
+            farq->push(first[k] && far[k], id[k], 0);
         }
     }
 };
@@ -193,13 +249,13 @@ __device__ __forceinline__ unsigned long long sssp_pull_step(const SsspArgs &a, 
             if ((best >> 32) < (cur >> 32)) {
                 a.dp[v] = best;  // v's owner: a plain 64-bit store
                 const bool far = (best >> 32) >= thr;
-                a.stamp[v] = key_near + (far ? 1 : 0);
+                a.stamp[v] = stamp_key(key_near, far);
                 if (far) to_far = true;
-                else { to_near = true; rs = a.R[v]; deg = a.R[v + 1] - rs; }
+                else { to_near = true; if (!nearq.Rl) { rs = a.R[v]; deg = a.R[v + 1] - rs; } }
                 ++nimp;
             }
         }
-        nearq.push(to_near && deg > 0, (int32_t)v, deg, rs);
+        nearq.push(to_near && (nearq.Rl || deg > 0), (int32_t)v, deg, rs);
         farq.push(to_far, (int32_t)v, 0);
     }
     return nimp;
@@ -259,7 +315,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
     nearq.overflow = &a.ctl->overflow;
     farq.sv = s->fv[wib]; farq.sd = nullptr; farq.cnt = 0; farq.qo = nullptr; farq.S = 0;
     nearq.stream = farq.stream = env_stream;
+    nearq.Rl = (a.lazy_r && !a.ellw) ? a.R : nullptr;
     farq.cap = a.far_cap; farq.overflow = &a.ctl->overflow;
+    farq.tag = 2;
     const unsigned long long pol_keep = policy_evict_last();
 
     uint64_t thr = a.delta;          // near band is [.., thr)
@@ -273,11 +331,11 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         Slot &nxt = a.ctl->slot[(k + 1) & 3];
         // ---- control words: one thread reads, the CTA shares ----------------
         if (threadIdx.x == 0) {
-            s->ctl[0] = ld_volatile(&cur.qpack);
-            s->ctl[1] = ld_volatile(&a.ctl->far_count[fp]);
-            s->ctl[2] = ld_volatile(&cur.ndisc);
-            s->ctl[3] = ld_volatile(&a.ctl->overflow);
-            s->ctl[5] = ld_volatile(&cur.dmax);
+            s->ctl[0] = ld_relaxed(&cur.qpack);
+            s->ctl[1] = ld_relaxed(&a.ctl->far_count[fp]);
+            s->ctl[2] = ld_relaxed(&cur.ndisc);
+            s->ctl[3] = ld_relaxed(&a.ctl->overflow);
+            s->ctl[5] = ld_relaxed(&cur.dmax);
             s->bsum[0] = 0;
         }
         __syncthreads();
@@ -315,7 +373,8 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             ++it;
             farq.qv = a.far[fp];
             farq.counter = &a.ctl->far_count[fp];
-            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep, policy_evict_first()};
+            RelaxOp op{a.dp, a.stamp, a.W, a.R, thr, 2 * it, &nearq, &farq, 0ull, pol_keep, policy_evict_first(),
+                       a.ellw};
             GlobalFrontier fr{a.qv[k & 1], a.qo[k & 1], a.qr[k & 1], f, mf};
             const bool pull = a.CWt && (a.direction == 2 || (a.direction == 0 && (double)mf * a.alpha > (double)a.m));
             if (pull && tid == 0 && k < kMaxStatRecords) a.stats[k].direction = 5;  // pull relax
@@ -331,6 +390,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
                 }
                 grid.sync();
                 op.nimp = sssp_pull_step(a, thr, 2 * it, gw, nw, nearq, farq, pol_keep);
+            } else if (a.ellw) {
+                // bounded-degree graphs: one vertex per lane, warps spread over the SMs
+                expand_ellw(a.qv[k & 1], f, a.ellw, (int64_t)wib * gridDim.x + blockIdx.x, nw, op);
             } else
             // same auto rule as BFS (reading A-4): short lists -> thread/warp/CTA
             if (f < a.lb_threshold && mf <= 16 * f && (int64_t)s->ctl[5] <= kTwcMaxDeg)  // no long list (see bfs.cu)
@@ -373,7 +435,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             __syncthreads();
             if (threadIdx.x == 0 && s->bsum[1] != ~0ull) atomicMin(&cur.minfar, s->bsum[1]);
             grid.sync();
-            if (threadIdx.x == 0) s->ctl[4] = ld_volatile(&cur.minfar);
+            if (threadIdx.x == 0) s->ctl[4] = ld_relaxed(&cur.minfar);
             if (tid == 0) a.ctl->far_count[fp] = 0ull;
             __syncthreads();
             const unsigned long long mn = s->ctl[4];
@@ -396,16 +458,17 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
                 if (j < fc) {
                     v = far_c[j];
                     const unsigned long long d = ld_probe(a.dp + v, pol_keep) >> 32;
+                    const int64_t r0 = nearq.Rl ? 0 : a.R[v], r1 = nearq.Rl ? 0 : a.R[v + 1];  // with d
                     if (d >= thr_old) {  // else stale: already expanded below thr_old
                         const bool nearb = d < thr;
-                        const int32_t key = 2 * it + (nearb ? 0 : 1);
-                        if (atomicExch(a.stamp + v, key) != key) {
-                            if (nearb) { to_near = true; rs = a.R[v]; deg = a.R[v + 1] - rs; }
+                        const int32_t key = stamp_key(2 * it, !nearb);
+                        if (atomicMax(a.stamp + v, key) < key) {
+                            if (nearb) { to_near = true; rs = r0; deg = r1 - r0; }
                             else to_far = true;
                         }
                     }
                 }
-                nearq.push(to_near && deg > 0, v, deg, rs);
+                nearq.push(to_near && (nearq.Rl || deg > 0), v, deg, rs);
                 farq.push(to_far, v, 0);
             }
             if (fc >= 16384) {
@@ -445,6 +508,8 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.n = g->n; a.m = g->m;
     a.R = g->R; a.C = g->C; a.W = g->W; a.CW = g->CW;
     a.Rt = g->Rt; a.CWt = g->CWt; a.fb = g->fbuf[0];
+    a.ellw = g->ellw;
+    a.lazy_r = (int32_t)env_int("GR_LAZY_R", 1);
     a.direction = direction;
     a.alpha = alpha > 0 ? alpha : 2.0;  // measured on C3: pull pays only when m_f > m / 2
     a.dp = g->dp; a.stamp = g->stamp;

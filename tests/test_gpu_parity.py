@@ -320,3 +320,42 @@ def test_mid_size_variants(gr, env, monkeypatch):
         _check_bfs(gr, G, g, gg.sources(g, 2), dirs=["push", "auto", "pull"])
         _check_bfs(gr, G, g, gg.sources(g, 1), dirs=["auto"], idempotent=True)
         G.close()
+
+
+# ------------------------------------------------------------------ bounded-degree adjacency
+
+def _bounded_directed(n, seed):
+    """Directed graph with out-degrees 0..4 (the ELL record's capacity) and
+    in-degrees unconstrained; weights 1..64."""
+    rng = np.random.default_rng(seed)
+    deg = rng.integers(0, 5, size=n)
+    src = np.repeat(np.arange(n), deg)
+    dst = rng.integers(0, n, size=src.size)
+    w = rng.integers(1, 65, size=src.size)
+    return gg.from_edges(n, list(zip(src.tolist(), dst.tolist())), w.tolist(), symmetrize=False)
+
+
+@pytest.mark.parametrize("ell", ["1", "0"])
+def test_bounded_degree_adjacency(gr, ell, monkeypatch):
+    """Graphs whose out-degrees are all <= 4 get the 16-B / 32-B per-vertex
+    adjacency records (gr_graph_info.bounded_degree); BFS in every direction
+    and mode, and SSSP for several deltas, equal the oracle with the records
+    (GR_ELL=1, default) and without them (GR_ELL=0)."""
+    monkeypatch.setenv("GR_ELL", ell)
+    graphs = [gg.assign_weights(gg.grid(61, 47), seed=3), gg.assign_weights(gg.path(3000), seed=4),
+              gg.make_config("c4_road", shrink=3), _bounded_directed(60000, 5),
+              gg.assign_weights(gg.binary_tree(20000), seed=6)]
+    for g in graphs:
+        G = _dev(g, gr)
+        info = G.info()
+        assert info.bounded_degree == (1 if ell == "1" else 0), (g.n, info.max_degree)
+        srcs = gg.sources(g, 2) + [0]
+        _check_bfs(gr, G, g, srcs)
+        _check_bfs(gr, G, g, srcs[:1], dirs=["push", "auto"], idempotent=True)
+        _check_sssp(gr, G, g, srcs[:2], deltas=[1, 8, 64, 0xFFFFFFFF, 0])
+        G.close()
+    # max out-degree 5: no records
+    g = gg.star(5)
+    G = _dev(g, gr)
+    assert G.info().bounded_degree == 0
+    G.close()
