@@ -76,6 +76,9 @@ struct BfsArgs {
     int32_t claim_cas;         // push claim: CAS on depth[] (1) or atomicOr on the bitmap (0)
     int64_t probe_skip_pct;    // push steps skip the culling probe while m_u >= this % of m
     int32_t lazy_r;            // grid push: row offsets of discovered vertices loaded at the flush
+    int32_t bar_ns;            // GridBar backoff cap (ns)
+    int32_t resume;            // bounded-degree graphs: the cluster kernel ran the first levels
+                               // (bfs_ell_cluster_kernel); continue from ctl->bstate, no init
 };
 
 template <int kNW>
@@ -448,7 +451,7 @@ template <int kBlk, int kMinB, bool kPush = false, bool kEll = false>
 __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
     constexpr int kNW = kBlk / kWarp;
     using BfsSmem = BfsSmemT<kNW>;
-    cg::grid_group grid = cg::this_grid();
+    const GridBar grid{&a.ctl->gbar, a.bar_ns};
     extern __shared__ __align__(128) unsigned char smem_raw[];
     BfsSmem *s = reinterpret_cast<BfsSmem *>(smem_raw);
     uint32_t *sbm_p = reinterpret_cast<uint32_t *>(smem_raw + bfs_sbm_offset<kBlk>());
@@ -463,6 +466,35 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
     const int64_t nwords = (a.n + 31) / 32;
     const unsigned long long cmask = (1ull << a.S) - 1;
 
+    BfsState st;
+    long long t_prev = 0;
+    if (kEll && a.resume) {
+        // the narrow first levels ran in bfs_ell_cluster_kernel: it either
+        // finished the traversal or left the frontier of level bstate[0] in
+        // the queue with its descriptor in the level's slot
+        if (threadIdx.x == 0) {
+            long long x[7];
+#pragma unroll
+            for (int k = 0; k < 7; ++k) x[k] = __ldcg(a.ctl->bstate + k);
+#pragma unroll
+            for (int k = 0; k < 7; ++k) s->ctl[k] = (unsigned long long)x[k];
+            s->ctl[7] = __ldcg(&a.ctl->handoff);
+        }
+        __syncthreads();
+        if (s->ctl[7] != 1ull) return;  // finished in cluster mode
+        st.L = (int)(long long)s->ctl[0];
+        st.dir = (int)(long long)s->ctl[1];
+        st.prev_dir = (int)(long long)s->ctl[2];
+        st.u_cnt = (long long)s->ctl[3];
+        st.m_u = (long long)s->ctl[4];
+        st.prev_f = (long long)s->ctl[5];
+        if (tid == 0) t_prev = (long long)s->ctl[6];
+        st.closed = st.L;
+        st.fb_valid = 0;
+        st.fbn_clean = 0;
+        st.q_valid = 1;
+        __syncthreads();
+    } else {
     // ---- Set_Problem_Data: depth = -1 (A-2), pred = -1, src -----
     for (int64_t v = tid; v < a.n; v += nthreads) {
         a.depth[v] = -1;
@@ -490,7 +522,6 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
     // Heuristic state. u = unvisited vertices that have an in-edge, m_u =
     // edges incident to them (reading A-3).
     const bool src_has_in = !((a.noin[a.src >> 5] >> (a.src & 31)) & 1u);
-    BfsState st;
     st.L = 0;
     st.dir = (a.direction == 2) ? 2 : 1;
     st.prev_dir = 1;
@@ -501,9 +532,9 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
     st.fbn_clean = 0;
     st.closed = 0;
     st.q_valid = 1;
-    const unsigned long long pol_keep = policy_evict_last();
-    long long t_prev = 0;
     if (tid == 0) t_prev = gtimer();
+    }
+    const unsigned long long pol_keep = policy_evict_last();
     bool pending = false;  // counters of the last grid level not yet applied to u, m_u
 
     Appender app;
@@ -852,6 +883,253 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Narrow levels of bounded-degree graphs in ONE thread-block cluster
+// (high-diameter graphs, C4: ~10.6K levels of a few hundred to ~8K
+// vertices). A level of the grid kernel is a chain of L2 round trips plus a
+// 296-CTA barrier (~8 us); here the frontier lives in the cluster's
+// distributed shared memory and a level costs one DSMEM read of the CTAs'
+// counters, the entry (DSMEM) and its ELL record, one batch of claims, a
+// shared-memory append and a hardware cluster barrier.
+//  * every CTA appends the vertices its threads discover to its own
+//    shared-memory queue (one packed (edges << 32) | count atomic per warp);
+//  * the next level's entry j is owned by the CTA whose count prefix covers
+//    j: each thread takes global index j = rank * 1024 + tid, so the work of
+//    a level is spread evenly over the cluster whatever CTA discovered it;
+//  * a level runs here only if its frontier fits one entry per thread
+//    (then no CTA can append more than 4 x 1024 entries) and the direction
+//    rule (A-3) says push; otherwise the frontier is written to the global
+//    queue and the grid kernel resumes at that level (Ctl::handoff, bstate).
+// Same semantics as the grid push step: atomicOr claim (exactly once),
+// depth = L + 1, pred = the frontier vertex.
+// ---------------------------------------------------------------------------
+constexpr int kClBlock = 1024;
+constexpr int kClQ = 4 * kClBlock;   // per-CTA queue: <= 4 appends per thread per level
+constexpr int kClMax = 16;
+
+struct ClSmem {
+    int32_t q[2][kClQ];               // appended vertices, by level parity
+    unsigned long long cnt[3];        // (edges << 32) | count appended, by level mod 3
+    unsigned long long nd[3];         // vertices discovered (degree 0 too), by level mod 3
+    int pfx[kClMax + 1];              // exclusive prefix of the CTAs' counts (current level)
+    long long tot[3];                 // F, MF, discovered by the previous level
+};
+
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_nctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long ld_dsmem_u64(const unsigned long long *p, unsigned rank) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    unsigned long long v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(r) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_dsmem_s32(const int32_t *p, unsigned rank) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    int32_t v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(r) : "memory");
+    return v;
+}
+
+// Set_Problem_Data for the cluster path: the whole GPU writes the
+// O(n) arrays; the cluster kernel then places the source.
+__global__ void bfs_init_kernel(BfsArgs a) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nwords = (a.n + 31) / 32;
+    for (int64_t v = tid; v < a.n; v += nthreads) {
+        a.depth[v] = -1;
+        if (a.pred) a.pred[v] = -1;
+    }
+    for (int64_t w = tid; w < nwords; w += nthreads) a.visited[w] = a.noin[w];
+    if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) ((unsigned long long *)a.ctl->slot)[tid] = 0ull;
+    if (tid == 0) { a.ctl->overflow = 0ull; a.ctl->handoff = 0ull; }
+}
+
+__global__ void __launch_bounds__(kClBlock, 1) bfs_ell_cluster_kernel(BfsArgs a) {
+    __shared__ ClSmem s;
+    const unsigned K = cluster_nctarank();
+    const unsigned rank = cluster_ctarank();
+    const int t = threadIdx.x;
+    const unsigned l = lane_id();
+    const int64_t nwords = (a.n + 31) / 32;
+    if (t < 3) { s.cnt[t] = 0ull; s.nd[t] = 0ull; }
+    const int64_t deg_src = a.R[a.src + 1] - a.R[a.src];
+    __syncthreads();
+    if (rank == 0 && t == 0) {
+        a.depth[a.src] = 0;
+        if (a.pred) a.pred[a.src] = a.src;  // A-1
+        atomicOr(a.visited + (a.src >> 5), 1u << (a.src & 31));
+        if (deg_src > 0) { s.q[0][0] = a.src; s.cnt[0] = ((unsigned long long)deg_src << 32) | 1ull; }
+    }
+    cluster_barrier();
+    const bool src_has_in = !((a.noin[a.src >> 5] >> (a.src & 31)) & 1u);
+    int64_t u_cnt = a.nonisolated - (src_has_in ? 1 : 0);
+    int64_t m_u = a.m - deg_src;
+    int64_t prev_f = 0;
+    long long tp = 0;
+    if (rank == 0 && t == 0) tp = gtimer();
+    int L = 0;
+    for (;;) {
+        const int c0 = L % 3, c1 = (L + 1) % 3, c2 = (L + 2) % 3, p = L & 1;
+        // ---- the level's counters from every CTA of the cluster (DSMEM) ----
+        if (t < 32) {
+            unsigned long long x = 0, y = 0;
+            if (l < K) { x = ld_dsmem_u64(&s.cnt[c0], l); y = ld_dsmem_u64(&s.nd[c0], l); }
+            const int cn = (int)(x & 0xffffffffu);
+            const int incl = warp_incl_scan<int>(cn);
+            const long long e = warp_sum<long long>((long long)(x >> 32));
+            const long long d = warp_sum<long long>((long long)y);
+            if (l < K) s.pfx[l + 1] = incl;
+            if (l == 0) { s.pfx[0] = 0; s.tot[1] = e; s.tot[2] = d; }
+            if (l == 31) s.tot[0] = incl;
+        }
+        __syncthreads();
+        const int64_t F = s.tot[0], MF = s.tot[1], ND = s.tot[2];
+        if (L > 0) { u_cnt -= ND; m_u -= MF; }
+        if (rank == 0 && t == 0 && L > 0 && L - 1 < kMaxStatRecords) {
+            const long long tn = gtimer();
+            a.stats[L - 1].discovered = ND;
+            a.stats[L - 1].ns = tn - tp;
+            tp = tn;
+        }
+        if (F == 0) {
+            if (rank == 0 && t == 0) { a.ctl->levels = (unsigned long long)L; a.ctl->handoff = 2ull; }
+            break;
+        }
+        const int dir = decide_direction(a, 1, F, MF, u_cnt, m_u, prev_f, nwords);
+        if (dir != 1 || F > (int64_t)K * kClBlock) {
+            // ---- hand the frontier of level L to the grid kernel ----------
+            for (int64_t j = (int64_t)t * K + rank; j < F; j += (int64_t)K * kClBlock) {
+                int o = 0;
+                while (o + 1 < (int)K && s.pfx[o + 1] <= j) ++o;
+                a.qv[L & 1][j] = ld_dsmem_s32(&s.q[p][j - s.pfx[o]], o);
+            }
+            if (rank == 0 && t == 0) {
+                a.ctl->slot[L & 3].qpack = ((unsigned long long)MF << a.S) | (unsigned long long)F;
+                a.ctl->slot[L & 3].dmax = 4ull;
+                a.ctl->slot[L & 3].ndisc = 0; a.ctl->slot[L & 3].insp = 0; a.ctl->slot[L & 3].work = 0;
+                for (int k = 1; k <= 2; ++k) {
+                    Slot &r = a.ctl->slot[(L + k) & 3];
+                    r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull; r.dmax = 0;
+                }
+                long long *bs = a.ctl->bstate;
+                bs[0] = L; bs[1] = 1; bs[2] = 1; bs[3] = u_cnt; bs[4] = m_u; bs[5] = prev_f; bs[6] = tp;
+                a.ctl->handoff = 1ull;
+            }
+            break;
+        }
+        if (rank == 0 && t == 0 && L < kMaxStatRecords) {
+            gr_level_stats &sr = a.stats[L];
+            sr.level = L; sr.direction = 1; sr.frontier = F; sr.frontier_edges = MF;
+            sr.discovered = 0; sr.inspected_edges = MF; sr.aux = u_cnt; sr.ns = 0;
+        }
+        // counters of level L+2 were last read at level L-1 (before its barrier)
+        if (t == 0) { s.cnt[c2] = 0ull; s.nd[c2] = 0ull; }
+        // ---- expand: global entry j of the level, one per thread -----------
+        // entries interleaved over the CTAs (j = t * K + rank): a narrow level
+        // spreads over every SM of the cluster (its scattered record loads,
+        // claims and stores are issue-limited per SM: with j = rank * 1024 + t
+        // a 2K-vertex level ran on two SMs, 6.2 us per level on C4)
+        const int64_t j = (int64_t)t * K + rank;
+        int32_t v = 0;
+        int4 rec = make_int4(-1, -1, -1, -1);
+        if (j < F) {
+            int o = 0;
+#pragma unroll 1
+            while (o + 1 < (int)K && s.pfx[o + 1] <= j) ++o;
+            v = ld_dsmem_s32(&s.q[p][j - s.pfx[o]], o);
+            rec = ld_ell(a.ell + v);
+        }
+        const int32_t sl[4] = {rec.x, rec.y, rec.z, rec.w};
+        uint32_t old[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t w = sl[k] >> 3;
+            old[k] = sl[k] >= 0 ? atomicOr(a.visited + (w >> 5), 1u << (w & 31)) : 0xffffffffu;
+        }
+        int na = 0, nd = 0;
+        long long ea = 0;
+        bool ap[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int32_t w = sl[k] >> 3;
+            const bool disc = !((old[k] >> (w & 31)) & 1u);
+            ap[k] = disc && (sl[k] & 7) != 0;
+            if (disc) {
+                a.depth[w] = L + 1;
+                if (a.pred) a.pred[w] = v;
+                ++nd;
+                if (ap[k]) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.ell + w));
+            }
+            na += ap[k];
+            ea += ap[k] ? (sl[k] & 7) : 0;
+        }
+        // one packed shared-memory atomic per warp reserves the slots and the edges
+        const int incl = warp_incl_scan<int>(na);
+        const long long etot = warp_sum<long long>(ea);
+        const int ndw = warp_sum<int>(nd);
+        unsigned long long base = 0;
+        if (l == 31 && incl > 0) base = atomicAdd(&s.cnt[c1], ((unsigned long long)etot << 32) | (unsigned)incl);
+        if (l == 0 && ndw > 0) atomicAdd(&s.nd[c1], (unsigned long long)ndw);
+        base = __shfl_sync(0xffffffffu, base, 31);
+        int pos = (int)(base & 0xffffffffu) + incl - na;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            if (ap[k]) s.q[p ^ 1][pos++] = sl[k] >> 3;
+        prev_f = F;
+        ++L;
+        cluster_barrier();
+    }
+    // no CTA may exit while another still reads its shared memory (the last
+    // level's counters, the handed-off queue): every CTA leaves the loop at
+    // the same level (identical decisions), then waits for the others here
+    cluster_barrier();
+}
+
+// Largest cluster (16, else 8) of bfs_ell_cluster_kernel CTAs the device can
+// run (0: none; GR_ELL_CLUSTER_SIZE forces one).
+static int ell_cluster_size() {
+    static int k = -1;
+    if (k >= 0) return k;
+    k = 0;
+    const int want = (int)env_int("GR_ELL_CLUSTER_SIZE", 0);
+    cudaFuncSetAttribute(bfs_ell_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c : {16, 8}) {
+        if (want > 0 && c != want) continue;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)c);
+        cfg.blockDim = dim3(kClBlock);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, bfs_ell_cluster_kernel, &cfg) == cudaSuccess && ncl >= 1) {
+            k = c;
+            break;
+        }
+    }
+    cudaGetLastError();  // an unsupported size leaves an error behind
+    return k;
+}
+
 gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr_bfs_opts &o,
                   int *launches) {
     BfsArgs a;
@@ -880,6 +1158,7 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.claim_cas = (int32_t)env_int("GR_CLAIM_CAS", 0);
     a.probe_skip_pct = env_int("GR_PROBE_SKIP_PCT", 75);
     a.lazy_r = (int32_t)env_int("GR_LAZY_R", 1);
+    a.bar_ns = (int32_t)env_int("GR_BAR_NS", 128);
     if (a.small_f > kSmallF) a.small_f = kSmallF;
 
     // Kernel variant: graphs whose bitmap no
@@ -920,11 +1199,37 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     int64_t ctas = (int64_t)g->num_sms * per_sm;
     const int64_t cap_ctas = env_int("GR_BFS_CTAS", 0);  // experiment: fewer persistent CTAs
     if (cap_ctas > 0 && cap_ctas < ctas) ctas = cap_ctas;
+    // bounded-degree graphs: the narrow levels run in one thread-block cluster
+    // (bfs_ell_cluster_kernel), the grid kernel resumes only if a frontier
+    // outgrows it or the direction rule turns to pull
+    int nl = 0;
+    a.resume = 0;
+    const int kcl = (g->ell && !use_snap && a.direction != 2 && env_int("GR_ELL_CLUSTER", 1)) ? ell_cluster_size() : 0;
+    if (kcl > 0) {
+        bfs_init_kernel<<<g->num_sms * 4, 512, 0, g->stream>>>(a);
+        GR_CUDA(cudaGetLastError());
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)kcl);
+        cfg.blockDim = dim3(kClBlock);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = g->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)kcl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        GR_CUDA(cudaLaunchKernelEx(&cfg, bfs_ell_cluster_kernel, a));
+        count_launch(2);
+        nl += 2;
+        a.resume = 1;
+    }
     dim3 grid((unsigned)ctas), blk(block);
     void *args[] = {&a};
     GR_CUDA(cudaLaunchCooperativeKernel(fn, grid, blk, args, smem, g->stream));
     count_launch();
-    *launches = 1;
+    *launches = nl + 1;
     return GR_OK;
 }
 

@@ -69,6 +69,40 @@ struct Ctl {
     long long bstate[8];           // small-mode handoff of the traversal state
     unsigned long long sticky;     // some run since the last gr_graph_sync overflowed
     unsigned long long epoch;      // partitioned runs: cross-rank barrier epochs used so far
+    unsigned int gbar;             // GridBar arrival word (any initial value; never reset)
+    unsigned int pad_gbar;
+    unsigned long long handoff;    // bounded-degree BFS: 1 the cluster kernel handed the traversal
+                                   // to the grid kernel (state in bstate), 2 it finished it
+};
+
+// Grid-wide barrier of the persistent kernels (replaces cg::grid_group::sync):
+// the same arrive (atom.add.release, the master's addend flips bit 31 once all
+// CTAs arrived) and acquire poll as cooperative groups, but the poll backs off
+// with __nanosleep. cg's tight poll keeps one load per CTA in flight on the
+// barrier word's L2 slice for the whole level; on narrow levels (C4: ~20 of
+// 296 CTAs work, the rest wait) that traffic delayed the working CTAs'
+// accesses to the same slice (measured per-level time).
+struct GridBar {
+    unsigned int *bar;
+    int max_ns;   // backoff cap (0: tight poll)
+    __device__ __forceinline__ void sync() const {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned int nb = (blockIdx.x == 0) ? 0x80000000u - (gridDim.x - 1) : 1u;
+            unsigned int old, cur;
+            asm volatile("atom.add.release.gpu.u32 %0,[%1],%2;" : "=r"(old) : "l"(bar), "r"(nb) : "memory");
+            int ns = 16;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.u32 %0,[%1];" : "=r"(cur) : "l"(bar) : "memory");
+                if ((old ^ cur) & 0x80000000u) break;
+                if (max_ns > 0) {
+                    __nanosleep(ns);
+                    ns = ns * 2 > max_ns ? max_ns : ns * 2;
+                }
+            }
+        }
+        __syncthreads();
+    }
 };
 
 struct Graph;

@@ -24,6 +24,7 @@ struct SsspArgs {
     const uint32_t *CWt;      // packed weighted in-lists (u << 7) | w(u,v), or null: no pull steps
     const int4 *ellw;         // bounded-degree weighted adjacency (null: none; Graph::ellw)
     int32_t lazy_r;           // near queue: row offsets loaded at the appender's flush
+    int32_t bar_ns;           // GridBar backoff cap (ns)
     uint32_t *fb;             // pull steps: bitmap of the near frontier [ceil(n/32)]
     int32_t direction;        // 0 auto, 1 push, 2 pull (near iterations; reading A-24)
     double alpha;             // auto: pull when m_f * alpha > m
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
     using RelaxOp = RelaxOpT<kPacked>;
     const int32_t *Cs = kPacked ? reinterpret_cast<const int32_t *>(a.CW) : a.C;  // the advance's edge stream
     const bool env_stream = a.stream_queues;
-    cg::grid_group grid = cg::this_grid();
+    const GridBar grid{&a.ctl->gbar, a.bar_ns};
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SsspSmem *s = reinterpret_cast<SsspSmem *>(smem_raw);
 
@@ -510,6 +511,7 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.Rt = g->Rt; a.CWt = g->CWt; a.fb = g->fbuf[0];
     a.ellw = g->ellw;
     a.lazy_r = (int32_t)env_int("GR_LAZY_R", 1);
+    a.bar_ns = (int32_t)env_int("GR_BAR_NS", 128);
     a.direction = direction;
     a.alpha = alpha > 0 ? alpha : 2.0;  // measured on C3: pull pays only when m_f > m / 2
     a.dp = g->dp; a.stamp = g->stamp;
