@@ -7,7 +7,12 @@
 
 namespace gr {
 
-constexpr int kPullList = 96;   // pull: per-warp candidate list (< 64 + 32 before a batch)
+#ifndef GR_PULL_Q
+#define GR_PULL_Q 2
+#endif
+constexpr int kPullQ = GR_PULL_Q;            // pull: candidates per lane per batch
+constexpr int kPullBatch = 32 * kPullQ;      // pull: candidates per batch
+constexpr int kPullList = kPullBatch + 32;   // pull: per-warp candidate list (< batch + 32 before a batch)
 #ifndef GR_PULL_GRAB
 #define GR_PULL_GRAB 4
 #endif
@@ -66,56 +71,56 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
     };
     auto fbit = [&](int32_t u) -> bool { return (fword(u) >> (u & 31)) & 1u; };
     int cnt = 0;  // warp-uniform
-    auto process = [&](int k) {  // candidates wl[0, k), k <= 64
-        int32_t v[2], par[2], u0[2];
-        int64_t beg[2], end[2];
-        bool fnd[2];
+    auto process = [&](int k) {  // candidates wl[0, k), k <= kPullBatch
+        int32_t v[kPullQ], par[kPullQ], u0[kPullQ];
+        int64_t beg[kPullQ], end[kPullQ];
+        bool fnd[kPullQ];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) v[q] = ((int)l + 32 * q < k) ? wl[l + 32 * q] : -1;
+        for (int q = 0; q < kPullQ; ++q) v[q] = ((int)l + 32 * q < k) ? wl[l + 32 * q] : -1;
         if (a.ph) {
             // pull head {first in-neighbour, in-degree}: one 8-byte load per
             // candidate (consecutive candidates -> coalesced) answers most of
             // them (in-lists are ordered by neighbour degree, hubs first);
             // only unresolved lists read their row offset
-            int2 h[2];
-            int64_t rt[2];
+            int2 h[kPullQ];
+            int64_t rt[kPullQ];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) h[q] = v[q] >= 0 ? __ldg(a.ph + v[q]) : make_int2(-1, 0);
+            for (int q = 0; q < kPullQ; ++q) h[q] = v[q] >= 0 ? __ldg(a.ph + v[q]) : make_int2(-1, 0);
             // row offsets loaded speculatively with the heads (candidates are
             // sorted: coalesced), so an unresolved list starts its scan one
             // dependent round trip earlier
 #pragma unroll
-            for (int q = 0; q < 2; ++q) rt[q] = v[q] >= 0 ? __ldg(a.Rt + v[q]) : 0;
-            uint32_t fw[2];
+            for (int q = 0; q < kPullQ; ++q) rt[q] = v[q] >= 0 ? __ldg(a.Rt + v[q]) : 0;
+            uint32_t fw[kPullQ];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kPullQ; ++q) {
                 u0[q] = h[q].x;
                 fw[q] = u0[q] >= 0 ? fword(u0[q]) : 0u;
             }
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kPullQ; ++q) {
                 fnd[q] = u0[q] >= 0 && ((fw[q] >> (u0[q] & 31)) & 1u);
                 par[q] = u0[q];
                 pc.insp += (u0[q] >= 0);
             }
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kPullQ; ++q) {
                 beg[q] = (!fnd[q] && h[q].y > 1) ? rt[q] : 0;
                 end[q] = beg[q] + h[q].y;
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kPullQ; ++q) {
                 beg[q] = v[q] >= 0 ? a.Rt[v[q]] : 0;
                 end[q] = v[q] >= 0 ? a.Rt[v[q] + 1] : 0;
             }
 #pragma unroll
-            for (int q = 0; q < 2; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Ct + beg[q], pol) : -1;
-            uint32_t fw[2];
+            for (int q = 0; q < kPullQ; ++q) u0[q] = beg[q] < end[q] ? ld_stream(a.Ct + beg[q], pol) : -1;
+            uint32_t fw[kPullQ];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) fw[q] = u0[q] >= 0 ? fword(u0[q]) : 0u;
+            for (int q = 0; q < kPullQ; ++q) fw[q] = u0[q] >= 0 ? fword(u0[q]) : 0u;
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < kPullQ; ++q) {
                 fnd[q] = u0[q] >= 0 && ((fw[q] >> (u0[q] & 31)) & 1u);
                 par[q] = u0[q];
                 pc.insp += (u0[q] >= 0);
@@ -125,9 +130,9 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
         // at most kPullLong edges), then what is left of the long ones by the
         // whole warp, 32 edges a step with a ballot early exit (one lane
         // scanning a long list alone held its warp for 100+ us on C3)
-        int64_t nxt[2];
+        int64_t nxt[kPullQ];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kPullQ; ++q) {
             nxt[q] = beg[q] + 1;
             if (fnd[q]) continue;
             const int64_t lim = (end[q] - nxt[q] > kPullLong) ? nxt[q] + kPullLong : end[q];
@@ -148,11 +153,11 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
             }
             nxt[q] = lim;
         }
-        bool lng[2];
+        bool lng[kPullQ];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) lng[q] = !fnd[q] && nxt[q] < end[q];
+        for (int q = 0; q < kPullQ; ++q) lng[q] = !fnd[q] && nxt[q] < end[q];
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kPullQ; ++q) {
             unsigned lm = __ballot_sync(0xffffffffu, lng[q]);
             while (lm) {
                 const int ld = __ffs(lm) - 1;
@@ -175,7 +180,7 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
             }
         }
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < kPullQ; ++q) {
             if (!fnd[q]) continue;
             const int32_t x = v[q];
             a.depth[x] = next_depth;
@@ -219,10 +224,10 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
             if ((w >> l) & 1u) wl[cnt + __popc(w & lanemask_lt())] = (int32_t)((w0 + j) * 32 + l);
             cnt += __popc(w);
             __syncwarp();
-            if (cnt >= 64) process(64);
+            if (cnt >= kPullBatch) process(kPullBatch);
         }
     }
-    while (cnt > 0) process(cnt < 64 ? cnt : 64);
+    while (cnt > 0) process(cnt < kPullBatch ? cnt : kPullBatch);
 }
 
 // Frontier bitmap -> queue (the other direction of the

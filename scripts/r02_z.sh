@@ -1,0 +1,6 @@
+#!/bin/bash
+OUT=gpurun_out/r02z; mkdir -p $OUT
+for lib in libgr_b200.so libgr_q1.so libgr_g8.so libgr_g2.so; do
+  GR_LIB=$lib timeout 600 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-extras > $OUT/c2_auto_$lib.json 2>/dev/null; echo "c2 auto $lib $?"
+  GR_LIB=$lib timeout 600 python scripts/levels.py --config c2_kron21 --directions auto --nsrc 1 > $OUT/levels_c2_$lib.txt 2>&1
+done
