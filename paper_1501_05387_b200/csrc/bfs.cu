@@ -904,9 +904,6 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
 // Same semantics as the grid push step: atomicOr claim (exactly once),
 // depth = L + 1, pred = the frontier vertex.
 // ---------------------------------------------------------------------------
-constexpr int kClBlock = 1024;
-constexpr int kClQ = 4 * kClBlock;   // per-CTA queue: <= 4 appends per thread per level
-constexpr int kClMax = 16;
 
 struct ClSmem {
     int32_t q[2][kClQ];               // appended vertices, by level parity
@@ -915,34 +912,6 @@ struct ClSmem {
     int pfx[kClMax + 1];              // exclusive prefix of the CTAs' counts (current level)
     long long tot[3];                 // F, MF, discovered by the previous level
 };
-
-__device__ __forceinline__ unsigned cluster_ctarank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ unsigned cluster_nctarank() {
-    unsigned r;
-    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_barrier() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ unsigned long long ld_dsmem_u64(const unsigned long long *p, unsigned rank) {
-    unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    unsigned long long v;
-    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(r) : "memory");
-    return v;
-}
-__device__ __forceinline__ int32_t ld_dsmem_s32(const int32_t *p, unsigned rank) {
-    unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    int32_t v;
-    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(r) : "memory");
-    return v;
-}
 
 // Set_Problem_Data for the cluster path: the whole GPU writes the
 // O(n) arrays; the cluster kernel then places the source.

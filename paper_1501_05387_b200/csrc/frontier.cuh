@@ -763,6 +763,43 @@ __device__ __forceinline__ void expand_twc(const Front &fr, const int32_t *__res
 }
 
 // ---------------------------------------------------------------------------
+// Thread-block cluster helpers of the narrow-level kernels (bfs.cu / sssp.cu
+// *_ell_cluster_kernel): one cluster of up to 16 CTAs x 1024 threads, the
+// frontier queues in distributed shared memory.
+// ---------------------------------------------------------------------------
+constexpr int kClBlock = 1024;
+constexpr int kClQ = 4 * kClBlock;   // per-CTA queue: <= 4 appends per thread per level
+constexpr int kClMax = 16;
+__device__ __forceinline__ unsigned cluster_ctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_nctarank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ unsigned long long ld_dsmem_u64(const unsigned long long *p, unsigned rank) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    unsigned long long v;
+    asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(r) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_dsmem_s32(const int32_t *p, unsigned rank) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(p), r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    int32_t v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(r) : "memory");
+    return v;
+}
+
+
+// ---------------------------------------------------------------------------
 // RemoveRedundant stamp of SSSP ("a bitmap flag array associated
 // with the frontier", reading A-7): the key of iteration `base` = 2*it and
 // slice is base + 1 for the near queue, base for the far pile, claimed with

@@ -25,6 +25,7 @@ struct SsspArgs {
     const int4 *ellw;         // bounded-degree weighted adjacency (null: none; Graph::ellw)
     int32_t lazy_r;           // near queue: row offsets loaded at the appender's flush
     int32_t bar_ns;           // GridBar backoff cap (ns)
+    int32_t resume;           // bounded-degree graphs: sssp_ell_cluster_kernel ran the first steps
     uint32_t *fb;             // pull steps: bitmap of the near frontier [ceil(n/32)]
     int32_t direction;        // 0 auto, 1 push, 2 pull (near iterations; reading A-24)
     double alpha;             // auto: pull when m_f * alpha > m
@@ -284,6 +285,31 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
     const int wib = threadIdx.x >> 5;
     const unsigned long long cmask = (1ull << a.S) - 1;
 
+    uint64_t thr = a.delta;          // near band is [.., thr)
+    int32_t it = 0;                  // stamp iteration (keys 2*it, 2*it+1)
+    int fp = 0;                      // current far buffer
+    int k = 0;                       // step index (slots, queue ping-pong)
+    long long t_prev = 0;
+    if (a.resume) {
+        // the narrow first steps ran in sssp_ell_cluster_kernel: finished, or
+        // the state of step bstate[0] handed over (queue, far piles, slots)
+        if (threadIdx.x == 0) {
+            long long x[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) x[q] = __ldcg(a.ctl->bstate + q);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) s->ctl[q] = (unsigned long long)x[q];
+            s->ctl[5] = __ldcg(&a.ctl->handoff);
+        }
+        __syncthreads();
+        if (s->ctl[5] != 1ull) return;
+        k = (int)(long long)s->ctl[0];
+        it = (int32_t)(long long)s->ctl[1];
+        thr = (uint64_t)s->ctl[2];
+        fp = (int)(long long)s->ctl[3];
+        if (tid == 0) t_prev = (long long)s->ctl[4];
+        __syncthreads();
+    } else {
     // ---- Set_Problem_Data ----------------------------------------
     for (int64_t v = tid; v < a.n; v += nthreads) {
         a.dp[v] = ~0ull;   // dist = UINT32_MAX (inf), pred = -1
@@ -309,6 +335,9 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         }
     }
     grid.sync();
+    if (tid == 0) t_prev = sssp_gtimer();
+    }
+    const int k0 = k;                // records below k0 were closed by the cluster kernel
 
     SsspAppender nearq, farq;
     nearq.sv = s->sv[wib]; nearq.sd = s->sd[wib]; nearq.sr = s->sr[wib]; nearq.cnt = 0; nearq.S = a.S;
@@ -321,12 +350,6 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
     farq.tag = 2;
     const unsigned long long pol_keep = policy_evict_last();
 
-    uint64_t thr = a.delta;          // near band is [.., thr)
-    int32_t it = 0;                  // stamp iteration (keys 2*it, 2*it+1)
-    int fp = 0;                      // current far buffer
-    int k = 0;                       // step index (slots, queue ping-pong)
-    long long t_prev = 0;
-    if (tid == 0) t_prev = sssp_gtimer();
     for (;; ++k) {
         Slot &cur = a.ctl->slot[k & 3];
         Slot &nxt = a.ctl->slot[(k + 1) & 3];
@@ -344,7 +367,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         const int64_t f = (int64_t)(qp & cmask);
         const int64_t mf = (int64_t)(qp >> a.S);
         const int64_t fc = (int64_t)s->ctl[1];
-        if (k > 0 && tid == 0 && k - 1 < kMaxStatRecords) {
+        if (k > k0 && tid == 0 && k - 1 < kMaxStatRecords) {
             a.stats[k - 1].discovered = (int64_t)s->ctl[2];
             const long long t = sssp_gtimer();
             a.stats[k - 1].ns = t - t_prev;
@@ -499,6 +522,307 @@ __global__ void unpack_kernel(const unsigned long long *dp, int64_t n, uint32_t 
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Narrow steps of bounded-degree SSSP in ONE thread-block cluster (the SSSP
+// counterpart of bfs_ell_cluster_kernel, bfs.cu): the near queue lives in the
+// cluster's distributed shared memory, the far piles stay in global memory;
+// a near iteration relaxes one frontier vertex per thread (entries
+// interleaved over the CTAs), a far re-split (A-11) reduces the minimum live
+// far distance over the cluster and splits the pile. The traversal is handed
+// to the grid kernel (sssp_kernel, resume) when a near frontier exceeds one
+// entry per thread, a far pile could overflow a CTA's queue, or the direction
+// rule (A-24) asks for a pull step. Semantics of the grid path: packed
+// (dist << 32 | pred) atomicMin (A-9) with strict improvement (RelaxOpT::
+// slots), monotone stamp keys (A-7), drop of stale far entries (A-11).
+// ---------------------------------------------------------------------------
+struct SClSmem {
+    int32_t q[2][kClQ];              // near queue appended by this CTA, by step parity
+    unsigned long long cnt[3];       // (edges << 32) | count near appends, by step mod 3
+    unsigned long long imp[3];       // improvements (stats), by step mod 3
+    unsigned long long mn;           // re-split: this CTA's minimum live far distance
+    int pfx[kClMax + 1];
+    long long tot[4];                // F, MF, improvements of the previous step, far count
+};
+
+__global__ void sssp_init_kernel(SsspArgs a) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < a.n; v += nthreads) {
+        a.dp[v] = ~0ull;   // dist = UINT32_MAX (inf), pred = -1
+        a.stamp[v] = -1;
+    }
+    if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) ((unsigned long long *)a.ctl->slot)[tid] = 0ull;
+    if (tid == 0) {
+        a.ctl->overflow = 0ull;
+        a.ctl->far_count[0] = 0ull;
+        a.ctl->far_count[1] = 0ull;
+        a.ctl->handoff = 0ull;
+    }
+}
+
+// warp-aggregated append of v into the global far pile fq (count *fc)
+__device__ __forceinline__ void cl_far_push(bool has, int32_t v, int32_t *fq, unsigned long long *fc, int64_t cap,
+                                            unsigned long long *overflow) {
+    const unsigned m = __ballot_sync(0xffffffffu, has);
+    if (!m) return;
+    unsigned long long base = 0;
+    if (lane_id() == 0) base = atomicAdd(fc, (unsigned long long)__popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (has) {
+        const unsigned long long pos = base + __popc(m & lanemask_lt());
+        if ((int64_t)pos < cap) fq[pos] = v;
+        else atomicExch(overflow, 2ull);
+    }
+}
+
+__global__ void __launch_bounds__(kClBlock, 1) sssp_ell_cluster_kernel(SsspArgs a) {
+    __shared__ SClSmem s;
+    const unsigned K = cluster_nctarank();
+    const unsigned rank = cluster_ctarank();
+    const int t = threadIdx.x;
+    const unsigned l = lane_id();
+    if (t < 3) { s.cnt[t] = 0ull; s.imp[t] = 0ull; }
+    const int64_t deg_src = a.R[a.src + 1] - a.R[a.src];
+    __syncthreads();
+    if (rank == 0 && t == 0) {
+        a.dp[a.src] = (unsigned long long)(unsigned int)a.src;  // dist 0, pred = src (A-1)
+        if (deg_src > 0) { s.q[0][0] = a.src; s.cnt[0] = ((unsigned long long)deg_src << 32) | 1ull; }
+    }
+    cluster_barrier();
+    uint64_t thr = a.delta;
+    int32_t it = 0;
+    int fp = 0;
+    long long tp = 0;
+    if (rank == 0 && t == 0) tp = sssp_gtimer();
+    const unsigned long long pol = policy_evict_last();
+    int k = 0;
+    for (;; ++k) {
+        const int c0 = k % 3, c1 = (k + 1) % 3, c2 = (k + 2) % 3, p = k & 1;
+        if (t < 32) {
+            unsigned long long x = 0, y = 0;
+            if (l < K) { x = ld_dsmem_u64(&s.cnt[c0], l); y = ld_dsmem_u64(&s.imp[c0], l); }
+            const int cn = (int)(x & 0xffffffffu);
+            const int incl = warp_incl_scan<int>(cn);
+            const long long e = warp_sum<long long>((long long)(x >> 32));
+            const long long d = warp_sum<long long>((long long)y);
+            if (l < K) s.pfx[l + 1] = incl;
+            if (l == 0) { s.pfx[0] = 0; s.tot[1] = e; s.tot[2] = d; s.tot[3] = (long long)__ldcg(&a.ctl->far_count[fp]); }
+            if (l == 31) s.tot[0] = incl;
+        }
+        __syncthreads();
+        const int64_t F = s.tot[0], MF = s.tot[1], NI = s.tot[2], fc = s.tot[3];
+        if (rank == 0 && t == 0 && k > 0 && k - 1 < kMaxStatRecords) {
+            const long long tn = sssp_gtimer();
+            a.stats[k - 1].discovered = NI;
+            a.stats[k - 1].ns = tn - tp;
+            tp = tn;
+        }
+        if (F == 0 && fc == 0) {
+            if (rank == 0 && t == 0) { a.ctl->levels = (unsigned long long)k; a.ctl->handoff = 2ull; }
+            break;
+        }
+        const bool pull = F > 0 && a.CWt && (a.direction == 2 || (a.direction == 0 && (double)MF * a.alpha > (double)a.m));
+        if ((F > 0 && (F > (int64_t)K * kClBlock || pull)) || (F == 0 && fc > (int64_t)K * kClQ)) {
+            // ---- hand the step to the grid kernel -------------------------
+            for (int64_t j = (int64_t)t * K + rank; j < F; j += (int64_t)K * kClBlock) {
+                int o = 0;
+                while (o + 1 < (int)K && s.pfx[o + 1] <= j) ++o;
+                a.qv[k & 1][j] = ld_dsmem_s32(&s.q[p][j - s.pfx[o]], o);
+            }
+            if (rank == 0 && t == 0) {
+                for (int q = 0; q < kSlots; ++q) {
+                    Slot &r = a.ctl->slot[q];
+                    r.qpack = 0; r.ndisc = 0; r.fpack = 0; r.work = 0; r.insp = 0; r.minfar = ~0ull; r.dmax = 0;
+                }
+                a.ctl->slot[k & 3].qpack = ((unsigned long long)MF << a.S) | (unsigned long long)F;
+                a.ctl->slot[k & 3].dmax = 4ull;
+                long long *bs = a.ctl->bstate;
+                bs[0] = k; bs[1] = it; bs[2] = (long long)thr; bs[3] = fp; bs[4] = tp;
+                a.ctl->handoff = 1ull;
+            }
+            break;
+        }
+        if (rank == 0 && t == 0 && k < kMaxStatRecords) {
+            gr_level_stats &st = a.stats[k];
+            st.level = k; st.direction = F > 0 ? 3 : 4; st.frontier = F > 0 ? F : fc;
+            st.frontier_edges = MF; st.discovered = 0; st.inspected_edges = MF; st.aux = fc; st.ns = 0;
+        }
+        if (t == 0) { s.cnt[c2] = 0ull; s.imp[c2] = 0ull; }
+        int na = 0;
+        long long ea = 0;
+        int32_t nv[4];
+        unsigned long long nimp = 0;
+        if (F > 0) {
+            // ---- near iteration: UpdateLabel + SetPred + RemoveRedundant ----
+            ++it;
+            const int64_t j = (int64_t)t * K + rank;
+            int32_t u = 0;
+            unsigned long long du = 0;
+            int4 id4 = make_int4(-1, -1, -1, -1), wt4 = make_int4(0, 0, 0, 0);
+            if (j < F) {
+                int o = 0;
+#pragma unroll 1
+                while (o + 1 < (int)K && s.pfx[o + 1] <= j) ++o;
+                u = ld_dsmem_s32(&s.q[p][j - s.pfx[o]], o);
+                du = ld_probe(a.dp + u, pol) >> 32;
+                id4 = ld_ell(a.ellw + 2 * (int64_t)u);
+                wt4 = ld_ell(a.ellw + 2 * (int64_t)u + 1);
+            }
+            const int32_t id[4] = {id4.x, id4.y, id4.z, id4.w};
+            const int32_t wt[4] = {wt4.x, wt4.y, wt4.z, wt4.w};
+            unsigned long long nd[4], old[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                nd[q] = du + (unsigned long long)((uint32_t)wt[q] >> 3);
+                old[q] = id[q] >= 0 ? atomicMin(a.dp + id[q], (nd[q] << 32) | 0xffffffffull) : 0ull;
+            }
+            bool imp[4], far[4];
+            int32_t ex[4];
+            const int32_t key_base = 2 * it;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                imp[q] = id[q] >= 0 && nd[q] < (old[q] >> 32);
+                if (imp[q]) atomicMin(a.dp + id[q], (nd[q] << 32) | (unsigned int)u);  // RED.MIN: the pred
+                far[q] = nd[q] >= thr;
+                const int32_t key = stamp_key(key_base, far[q]);
+                ex[q] = imp[q] ? atomicMax(a.stamp + id[q], key) : key;
+                nimp += imp[q];
+            }
+            bool tofar[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool first = imp[q] && ex[q] < stamp_key(key_base, far[q]);
+                const int32_t deg = wt[q] & 7;
+                const bool tonear = first && !far[q] && deg > 0;
+                tofar[q] = first && far[q];
+                nv[q] = tonear ? id[q] : -1;
+                na += tonear;
+                ea += tonear ? deg : 0;
+                if (tonear) {  // the next iteration reads its record and its distance
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.ellw + 2 * (int64_t)id[q]));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(a.dp + id[q]));
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                cl_far_push(tofar[q], id[q], a.far[fp], &a.ctl->far_count[fp], a.far_cap, &a.ctl->overflow);
+        } else {
+            // ---- far re-split (A-11): minimum live far distance, then split --
+            const int32_t *far_c = a.far[fp];
+            unsigned long long mymin = ~0ull;
+            for (int64_t j = (int64_t)t * K + rank; j < fc; j += (int64_t)K * kClBlock) {
+                const unsigned long long d = ld_probe(a.dp + far_c[j], pol) >> 32;
+                if (d >= thr && d < mymin) mymin = d;
+            }
+#pragma unroll
+            for (int sh = 16; sh > 0; sh >>= 1) {
+                const unsigned long long o = __shfl_xor_sync(0xffffffffu, mymin, sh);
+                mymin = o < mymin ? o : mymin;
+            }
+            if (t == 0) s.mn = ~0ull;
+            __syncthreads();
+            if (l == 0 && mymin != ~0ull) atomicMin(&s.mn, mymin);
+            cluster_barrier();
+            if (t < 32) {
+                unsigned long long x = (l < K) ? ld_dsmem_u64(&s.mn, l) : ~0ull;
+#pragma unroll
+                for (int sh = 16; sh > 0; sh >>= 1) {
+                    const unsigned long long o = __shfl_xor_sync(0xffffffffu, x, sh);
+                    x = o < x ? o : x;
+                }
+                if (l == 0) s.tot[0] = (long long)x;
+            }
+            __syncthreads();
+            const unsigned long long mn = (unsigned long long)s.tot[0];
+            cluster_barrier();  // every CTA read every s.mn before it is reused
+            if (rank == 0 && t == 0) a.ctl->far_count[fp] = 0ull;  // consumed below (all read fc)
+            if (mn != ~0ull) {
+                const uint64_t thr_old = thr;
+                const uint64_t band = mn / a.delta + 1;
+                thr = (band > (0xFFFFFFFFFFFFFFFFull / a.delta)) ? 0xFFFFFFFFFFFFFFFFull : band * a.delta;
+                ++it;
+                const int32_t key_base = 2 * it;
+                for (int64_t j0 = 0; j0 < fc; j0 += (int64_t)K * kClBlock) {  // warp-uniform trip count
+                    const int64_t j = j0 + (int64_t)t * K + rank;
+                    bool tonear = false, tofar = false;
+                    int32_t v = 0;
+                    int64_t deg = 0;
+                    if (j < fc) {
+                        v = far_c[j];
+                        const unsigned long long d = ld_probe(a.dp + v, pol) >> 32;
+                        const int64_t r0 = a.R[v], r1 = a.R[v + 1];
+                        if (d >= thr_old) {  // else stale: already expanded below thr_old
+                            const bool nearb = d < thr;
+                            const int32_t key = stamp_key(key_base, !nearb);
+                            if (atomicMax(a.stamp + v, key) < key) {
+                                deg = r1 - r0;
+                                tonear = nearb && deg > 0;
+                                tofar = !nearb;
+                            }
+                        }
+                    }
+                    // near entries of a re-split: appended right here (<= 4 per thread: fc <= 4 x threads)
+                    const int incl = warp_incl_scan<int>(tonear ? 1 : 0);
+                    const long long et = warp_sum<long long>(tonear ? deg : 0);
+                    unsigned long long base = 0;
+                    if (l == 31 && incl > 0) base = atomicAdd(&s.cnt[c1], ((unsigned long long)et << 32) | (unsigned)incl);
+                    base = __shfl_sync(0xffffffffu, base, 31);
+                    if (tonear) s.q[p ^ 1][(int)(base & 0xffffffffu) + incl - 1] = v;
+                    cl_far_push(tofar, v, a.far[fp ^ 1], &a.ctl->far_count[fp ^ 1], a.far_cap, &a.ctl->overflow);
+                }
+            }
+            fp ^= 1;
+        }
+        // near appends of the iteration: one packed shared-memory atomic per warp
+        if (F > 0) {
+            const int incl = warp_incl_scan<int>(na);
+            const long long etot = warp_sum<long long>(ea);
+            unsigned long long base = 0;
+            if (l == 31 && incl > 0) base = atomicAdd(&s.cnt[c1], ((unsigned long long)etot << 32) | (unsigned)incl);
+            base = __shfl_sync(0xffffffffu, base, 31);
+            int pos = (int)(base & 0xffffffffu) + incl - na;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (nv[q] >= 0) s.q[p ^ 1][pos++] = nv[q];
+        }
+        const unsigned long long nw = warp_sum<unsigned long long>(nimp);
+        if (l == 0 && nw) atomicAdd(&s.imp[c1], nw);
+        cluster_barrier();
+    }
+    cluster_barrier();  // no CTA exits while another reads its shared memory
+}
+
+// Largest cluster (16, else 8) of sssp_ell_cluster_kernel CTAs the device
+// can run (0: none; GR_ELL_CLUSTER_SIZE forces one).
+static int sssp_cluster_size() {
+    static int k = -1;
+    if (k >= 0) return k;
+    k = 0;
+    const int want = (int)env_int("GR_ELL_CLUSTER_SIZE", 0);
+    cudaFuncSetAttribute(sssp_ell_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    for (int c : {16, 8}) {
+        if (want > 0 && c != want) continue;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)c);
+        cfg.blockDim = dim3(kClBlock);
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)c;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, sssp_ell_cluster_kernel, &cfg) == cudaSuccess && ncl >= 1) {
+            k = c;
+            break;
+        }
+    }
+    cudaGetLastError();
+    return k;
+}
+
 gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_t delta, int32_t direction,
                    double alpha, int *launches) {
     if (direction != 1 && !g->CWt) {  // weighted in-lists for pull steps, built on first use
@@ -538,13 +862,37 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     int64_t ctas = (int64_t)g->num_sms * per_sm;
     const int64_t cap_ctas = env_int("GR_SSSP_CTAS", 0);  // experiment: fewer persistent CTAs
     if (cap_ctas > 0 && cap_ctas < ctas) ctas = cap_ctas;
+    // bounded-degree graphs: the narrow steps run in one thread-block cluster
+    // (sssp_ell_cluster_kernel); the grid kernel resumes only if they outgrow it
+    int nl = 0;
+    a.resume = 0;
+    const int kcl = (g->ellw && direction != 2 && env_int("GR_ELL_CLUSTER", 1)) ? sssp_cluster_size() : 0;
+    if (kcl > 0) {
+        sssp_init_kernel<<<g->num_sms * 4, 512, 0, g->stream>>>(a);
+        GR_CUDA(cudaGetLastError());
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)kcl);
+        cfg.blockDim = dim3(kClBlock);
+        cfg.stream = g->stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = (unsigned)kcl;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        GR_CUDA(cudaLaunchKernelEx(&cfg, sssp_ell_cluster_kernel, a));
+        count_launch(2);
+        nl += 2;
+        a.resume = 1;
+    }
     dim3 grid((unsigned)ctas), block(kBlock);
     void *args[] = {&a};
     GR_CUDA(cudaLaunchCooperativeKernel(fn, grid, block, args, smem, g->stream));
     unpack_kernel<<<g->num_sms * 4, 256, 0, g->stream>>>(g->dp, g->n, dist, pred);
     GR_CUDA(cudaGetLastError());
     count_launch(2);
-    *launches = 2;
+    *launches = nl + 2;
     return GR_OK;
 }
 

@@ -25,6 +25,22 @@ bench)
   b c4_sssp --config c4_road --prim sssp --steps 2 --no-extras
   b c5 --config c5_kron25 --steps 8 --no-extras --cpu-sample-s 10
   ;;
+more)
+  b c5_part --partitioned --steps 8 --no-extras
+  b c3_part_sssp --partitioned --config c3_orkut --prim sssp --steps 4 --no-extras
+  b c2_bc --prim bc --steps 5 --no-extras
+  b c2_cc --prim cc --steps 5 --no-extras
+  b c2_pr --prim pr --steps 3 --no-extras
+  timeout 600 python scripts/level_hist.py c4_road bfs > $OUT/level_hist_c4_bfs.txt 2>&1
+  timeout 600 python scripts/level_hist.py c4_road sssp > $OUT/level_hist_c4_sssp.txt 2>&1
+  timeout 600 python scripts/levels.py --config c2_kron21 --directions auto,push --nsrc 2 > $OUT/levels_c2.txt 2>&1
+  ;;
+ncu_c4)
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:bfs_ell_cluster_kernel -s 1 -c 1 \
+     -o $OUT/prof_c4_bfs_cluster python bench.py --config c4_road --steps 1 --warmup 1 --no-cpu-baseline --no-extras \
+     > $OUT/ncu_c4_bfs.log 2>&1; echo "ncu c4 bfs rc=$?"
+  python scripts/ncu_summary.py $OUT/prof_c4_bfs_cluster.ncu-rep $OUT/ncu_c4_bfs_cluster_kernel.txt
+  ;;
 configs)
   timeout 1500 python -m pytest tests -m "gpu and slow" -x -q > $OUT/configs_tests.log 2>&1; echo "configs rc=$?"; tail -5 $OUT/configs_tests.log
   ;;
