@@ -815,6 +815,8 @@ def main():
         r["m"] = m
     byts = [algorithmic_bytes(r, n, args.prim, packed) for r in recs]
     kname = "bfs_kernel" if args.prim == "bfs" else "sssp_kernel"
+    if G.info().bounded_degree:  # narrow levels in one cluster; the grid kernel resumes only if they outgrow it
+        kname = ("bfs" if args.prim == "bfs" else "sssp") + "_ell_cluster_kernel (+ init, + resumed grid kernel)"
     achieved = sum(byts) / (tot_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_source": peak_src,

@@ -335,16 +335,22 @@ def _bounded_directed(n, seed):
     return gg.from_edges(n, list(zip(src.tolist(), dst.tolist())), w.tolist(), symmetrize=False)
 
 
-@pytest.mark.parametrize("ell", ["1", "0"])
-def test_bounded_degree_adjacency(gr, ell, monkeypatch):
+@pytest.mark.parametrize("ell,cluster", [("1", "1"), ("1", "0"), ("0", "1")])
+def test_bounded_degree_adjacency(gr, ell, cluster, monkeypatch):
     """Graphs whose out-degrees are all <= 4 get the 16-B / 32-B per-vertex
     adjacency records (gr_graph_info.bounded_degree); BFS in every direction
     and mode, and SSSP for several deltas, equal the oracle with the records
-    (GR_ELL=1, default) and without them (GR_ELL=0)."""
+    and the narrow levels in one thread-block cluster (default), with the
+    records on the grid kernel only (GR_ELL_CLUSTER=0), and without records
+    (GR_ELL=0). The 2^18-vertex tree's frontiers outgrow the cluster (one
+    entry per thread) and its delta=1 far piles outgrow its queues: both hand
+    the traversal to the grid kernel mid-run."""
     monkeypatch.setenv("GR_ELL", ell)
+    monkeypatch.setenv("GR_ELL_CLUSTER", cluster)
     graphs = [gg.assign_weights(gg.grid(61, 47), seed=3), gg.assign_weights(gg.path(3000), seed=4),
               gg.make_config("c4_road", shrink=3), _bounded_directed(60000, 5),
-              gg.assign_weights(gg.binary_tree(20000), seed=6)]
+              gg.assign_weights(gg.binary_tree(20000), seed=6),
+              gg.assign_weights(gg.binary_tree(1 << 18), seed=7)]
     for g in graphs:
         G = _dev(g, gr)
         info = G.info()
