@@ -495,27 +495,29 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
         st.q_valid = 1;
         __syncthreads();
     } else {
-    // ---- Set_Problem_Data: depth = -1 (A-2), pred = -1, src -----
+    // ---- Set_Problem_Data: depth = -1 (A-2), pred = -1, and the
+    // source's entries written by the thread that owns them in the same pass
+    // (one grid barrier instead of init-barrier-source-barrier) -------------
+    const int64_t deg_src = a.R[a.src + 1] - a.R[a.src];
     for (int64_t v = tid; v < a.n; v += nthreads) {
-        a.depth[v] = -1;
-        if (a.pred) a.pred[v] = -1;
+        a.depth[v] = (v == a.src) ? 0 : -1;
+        if (a.pred) a.pred[v] = (v == a.src) ? a.src : -1;  // A-1
     }
     // vertices with no in-edge can never be discovered: pre-mark them visited
     // so pull skips them (they keep depth -1; the bitmap is internal)
-    for (int64_t w = tid; w < nwords; w += nthreads) a.visited[w] = a.noin[w];
-    if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) ((unsigned long long *)a.ctl->slot)[tid] = 0ull;
-    if (tid == 0) a.ctl->overflow = 0ull;
-    grid.sync();
-    const int64_t deg_src = a.R[a.src + 1] - a.R[a.src];
+    for (int64_t w = tid; w < nwords; w += nthreads)
+        a.visited[w] = a.noin[w] | ((w == (a.src >> 5)) ? 1u << (a.src & 31) : 0u);
+    if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) {
+        unsigned long long x = 0ull;  // slot 0 (words 0 and 6): the source's frontier descriptor
+        if (tid == 0 && deg_src > 0) x = ((unsigned long long)deg_src << a.S) | 1ull;
+        if (tid == (int64_t)(offsetof(Slot, dmax) / 8)) x = (unsigned long long)deg_src;
+        ((unsigned long long *)a.ctl->slot)[tid] = x;
+    }
     if (tid == 0) {
-        a.depth[a.src] = 0;
-        if (a.pred) a.pred[a.src] = a.src;  // A-1
-        a.visited[a.src >> 5] |= 1u << (a.src & 31);
+        a.ctl->overflow = 0ull;
         a.qv[0][0] = a.src;
         a.qo[0][0] = 0;
         a.qr[0][0] = a.R[a.src];
-        a.ctl->slot[0].qpack = (deg_src > 0) ? (((unsigned long long)deg_src << a.S) | 1ull) : 0ull;
-        a.ctl->slot[0].dmax = (unsigned long long)deg_src;
     }
     grid.sync();
 
@@ -697,6 +699,15 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
                     bs[0] = st.L; bs[1] = st.dir; bs[2] = st.prev_dir; bs[3] = st.u_cnt;
                     bs[4] = st.m_u; bs[5] = st.prev_f; bs[6] = tp;
                 }
+            } else if (gridDim.x > 1) {
+                // the idle CTAs zero the three frontier bitmaps meanwhile, so
+                // the grid level that follows records its next frontier in a
+                // clean bitmap (a push -> pull switch then needs no
+                // queue -> bitmap conversion pass and its two grid barriers)
+                const int64_t nb = (int64_t)(gridDim.x - 1) * blockDim.x;
+                for (int64_t w = (int64_t)(blockIdx.x - 1) * blockDim.x + threadIdx.x; w < nwords; w += nb) {
+                    a.fbuf[0][w] = 0u; a.fbuf[1][w] = 0u; a.fbuf[2][w] = 0u;
+                }
             }
             grid.sync();
             if (threadIdx.x == 0) {
@@ -718,7 +729,7 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
             if (tid == 0) t_prev = (long long)s->ctl[6];
             st.closed = st.L;      // records below st.L are closed
             st.fb_valid = 0;       // small mode keeps no frontier bitmap
-            st.fbn_clean = 0;
+            st.fbn_clean = gridDim.x > 1 ? 1 : 0;  // zeroed by the idle CTAs above
             st.q_valid = 1;
             pending = false;
             __syncthreads();
