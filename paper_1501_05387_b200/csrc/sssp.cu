@@ -310,28 +310,29 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
         if (tid == 0) t_prev = (long long)s->ctl[4];
         __syncthreads();
     } else {
-    // ---- Set_Problem_Data ----------------------------------------
+    // ---- Set_Problem_Data, the source's entries written by their
+    // owner thread in the same pass: one grid barrier ----------------------
+    const int64_t d_src = a.R[a.src + 1] - a.R[a.src];
     for (int64_t v = tid; v < a.n; v += nthreads) {
-        a.dp[v] = ~0ull;   // dist = UINT32_MAX (inf), pred = -1
+        // dist = UINT32_MAX (inf), pred = -1; the source: dist 0, pred = src (A-1)
+        a.dp[v] = (v == a.src) ? (unsigned long long)(unsigned int)a.src : ~0ull;
         a.stamp[v] = -1;
     }
-    if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) ((unsigned long long *)a.ctl->slot)[tid] = 0ull;
+    if (tid < kSlots * (int64_t)(sizeof(Slot) / 8)) {
+        const int64_t word = tid % (int64_t)(sizeof(Slot) / 8);
+        unsigned long long x = word == (int64_t)(offsetof(Slot, minfar) / 8) ? ~0ull : 0ull;
+        if (tid == 0 && d_src > 0) x = ((unsigned long long)d_src << a.S) | 1ull;          // slot 0 qpack
+        if (tid == (int64_t)(offsetof(Slot, dmax) / 8) && d_src > 0) x = (unsigned long long)d_src;
+        ((unsigned long long *)a.ctl->slot)[tid] = x;
+    }
     if (tid == 0) {
         a.ctl->overflow = 0ull;
         a.ctl->far_count[0] = 0ull;
         a.ctl->far_count[1] = 0ull;
-    }
-    grid.sync();
-    if (tid < kSlots) a.ctl->slot[tid].minfar = ~0ull;
-    if (tid == 0) {
-        const int64_t d = a.R[a.src + 1] - a.R[a.src];
-        a.dp[a.src] = (unsigned long long)(unsigned int)a.src;  // dist 0, pred = src (A-1)
-        if (d > 0) {
+        if (d_src > 0) {
             a.qv[0][0] = a.src;
             a.qo[0][0] = 0;
             a.qr[0][0] = a.R[a.src];
-            a.ctl->slot[0].qpack = ((unsigned long long)d << a.S) | 1ull;
-            a.ctl->slot[0].dmax = (unsigned long long)d;
         }
     }
     grid.sync();
