@@ -21,6 +21,10 @@ constexpr int kPullGrab = GR_PULL_GRAB;  // pull: bitmap words per grab
 #define GR_PULL_LONG 4
 #endif
 constexpr int64_t kPullLong = GR_PULL_LONG;  // pull: longer unresolved in-lists are scanned by the warp
+#ifndef GR_PULL_SCAN_U
+#define GR_PULL_SCAN_U 1  // 4 and 8 measured slower (C2 0.130 -> 0.134 / 0.149 ms)
+#endif
+constexpr int kPullScanU = GR_PULL_SCAN_U;   // pull: 32-edge groups per warp-scan step
 
 // ---------------------------------------------------------------------------
 // Pull (bottom-up) step over in-edges: "pull starts with a
@@ -165,16 +169,33 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
                 const int64_t b = __shfl_sync(0xffffffffu, nxt[q], ld);
                 const int64_t e = __shfl_sync(0xffffffffu, end[q], ld);
                 int32_t hitu = -1;
-                for (int64_t x = b; x < e; x += 32) {
-                    const int32_t u = (x + l < e) ? ld_stream(a.Ct + x + l, pol) : -1;
-                    const bool hit = u >= 0 && fbit(u);
-                    const unsigned bm = __ballot_sync(0xffffffffu, hit);
-                    const int first = bm ? __ffs(bm) - 1 : 32;
-                    pc.insp += (u >= 0 && (int)l <= first);
-                    if (bm) {
-                        hitu = __shfl_sync(0xffffffffu, u, first);
-                        break;
+                // kPullScanU x 32 edges per step, all loads of a step in flight
+                // (one lane's unresolved long list was a chain of 2 dependent
+                // round trips per 32 edges: the pull level's tail warp)
+                for (int64_t x = b; x < e; x += 32 * kPullScanU) {
+                    int32_t u[kPullScanU];
+                    uint32_t uw[kPullScanU];
+#pragma unroll
+                    for (int k = 0; k < kPullScanU; ++k) {
+                        const int64_t y = x + 32 * k + l;
+                        u[k] = y < e ? ld_stream(a.Ct + y, pol) : -1;
                     }
+#pragma unroll
+                    for (int k = 0; k < kPullScanU; ++k) uw[k] = u[k] >= 0 ? fword(u[k]) : 0u;
+                    bool done = false;
+#pragma unroll
+                    for (int k = 0; k < kPullScanU; ++k) {
+                        if (done) break;
+                        const bool hit = u[k] >= 0 && ((uw[k] >> (u[k] & 31)) & 1u);
+                        const unsigned bm = __ballot_sync(0xffffffffu, hit);
+                        const int first = bm ? __ffs(bm) - 1 : 32;
+                        pc.insp += (u[k] >= 0 && (int)l <= first);
+                        if (bm) {
+                            hitu = __shfl_sync(0xffffffffu, u[k], first);
+                            done = true;
+                        }
+                    }
+                    if (done) break;
                 }
                 if ((int)l == ld && hitu >= 0) { fnd[q] = true; par[q] = hitu; }
             }
