@@ -21,6 +21,9 @@ constexpr int kPullGrab = GR_PULL_GRAB;  // pull: bitmap words per grab
 #define GR_PULL_LONG 4
 #endif
 constexpr int64_t kPullLong = GR_PULL_LONG;  // pull: longer unresolved in-lists are scanned by the warp
+#ifndef GR_PULL_AGG
+#define GR_PULL_AGG 0  // warp-aggregated REDs: C2 -0.7%, C3 -0.3%, C5 +1.3% (noise): off
+#endif
 #ifndef GR_PULL_SCAN_U
 #define GR_PULL_SCAN_U 1  // 4 and 8 measured slower (C2 0.130 -> 0.134 / 0.149 ms)
 #endif
@@ -202,13 +205,33 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
         }
 #pragma unroll
         for (int q = 0; q < kPullQ; ++q) {
+#if GR_PULL_AGG
+            // the batch's candidates are sorted: its found vertices share a few
+            // bitmap words; one RED per word and bitmap (warp OR-reduction)
+            {
+                const int32_t xw = v[q] >= 0 ? (v[q] >> 5) : -1;
+                unsigned rem = __ballot_sync(0xffffffffu, fnd[q]);
+                while (rem) {
+                    const int w0 = __shfl_sync(0xffffffffu, xw, __ffs(rem) - 1);
+                    const bool in = fnd[q] && xw == w0;
+                    const unsigned bits = __reduce_or_sync(0xffffffffu, in ? 1u << (v[q] & 31) : 0u);
+                    if ((int)l == __ffs(rem) - 1) {
+                        atomicOr(fnext + w0, bits);      // RED.OR
+                        atomicOr(a.visited + w0, bits);  // RED.OR
+                    }
+                    rem &= ~__ballot_sync(0xffffffffu, in);
+                }
+            }
+#endif
             if (!fnd[q]) continue;
             const int32_t x = v[q];
             a.depth[x] = next_depth;
             if (a.pred) a.pred[x] = par[q];
+#if !GR_PULL_AGG
             const uint32_t bit = 1u << (x & 31);
             atomicOr(fnext + (x >> 5), bit);      // RED.OR
             atomicOr(a.visited + (x >> 5), bit);  // RED.OR
+#endif
             const int64_t deg = sym ? end[q] - beg[q] : a.R[x + 1] - a.R[x];
             ++pc.ndisc;
             if (deg > 0) {
