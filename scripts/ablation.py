@@ -104,6 +104,35 @@ def run_dir(cfg, prim, nsrc, reps):
     return dict(config=cfg, prim=prim, n=g.n, m=g.m, rows=rows)
 
 
+def run_ell(cfg, nsrc):
+    """Bounded-degree graphs: CSR-only grid kernel vs the
+    ELL records on the grid kernel vs ELL + the one-cluster narrow levels."""
+    g = gg.make_config(cfg, device="cuda", weights=True)
+    srcs = gg.sources(g, nsrc)
+    rows = []
+    for name, ell, cl in (("CSR, grid kernel", "0", "0"), ("ELL records, grid kernel", "1", "0"),
+                          ("ELL records, cluster mode", "1", "1")):
+        os.environ["GR_ELL"] = ell
+        os.environ["GR_ELL_CLUSTER"] = cl
+        G = gr.Graph(g.R, g.C, g.W, symmetric=True)
+        for prim in ("bfs", "sssp"):
+            ms, edges, steps = 0.0, 0, 0
+            for s in srcs:
+                one = (lambda: G.bfs(s)) if prim == "bfs" else (lambda: G.sssp(s))
+                one()
+                ms += timed(one)
+                st = G.run_stats()
+                steps += st["num_levels"]
+                edges += st["reached_edges"]
+            k = len(srcs)
+            rows.append(dict(variant="%s %s" % (prim, name), ms=ms / k, gteps=edges / (ms * 1e-3) / 1e9,
+                             steps=steps / k, us_per_step=ms * 1e3 / steps))
+        G.close()
+    os.environ.pop("GR_ELL", None)
+    os.environ.pop("GR_ELL_CLUSTER", None)
+    return dict(config=cfg, prim="ell", n=g.n, m=g.m, rows=rows)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="c2_kron21,c3_orkut,c4_road")
@@ -139,6 +168,15 @@ def main():
             for row in r["rows"]:
                 print("| %s | %.3f | %.1f | %.1f | %.1f |" % (row["variant"], row["ms"], row["gteps"],
                                                            row["pull_steps"], row["steps"]))
+        if cfg == "c4_road":
+            r = run_ell(cfg, 2)
+            res.append(r)
+            print("\n### %s bounded-degree paths (records, cluster mode)\n" % cfg)
+            print("| variant | ms | GTEPS | steps | us / step |")
+            print("|---|---|---|---|---|")
+            for row in r["rows"]:
+                print("| %s | %.2f | %.3f | %.0f | %.2f |" % (row["variant"], row["ms"], row["gteps"], row["steps"],
+                                                          row["us_per_step"]))
         sys.stdout.flush()
     if a.out:
         with open(a.out, "w") as f:
