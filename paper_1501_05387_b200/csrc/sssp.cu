@@ -46,9 +46,11 @@ struct SsspArgs {
     int S;
 };
 
-constexpr int kSsspStages = 2;     // cp.async pipeline depth (C + W + payload per stage)
 #ifndef GR_SSSP_PIPE
 #define GR_SSSP_PIPE 0  // cp.async pipeline off: its shared memory displaces L1 (measured slower)
+#endif
+#if GR_SSSP_PIPE
+constexpr int kSsspStages = 2;     // cp.async pipeline depth (C + W + payload per stage)
 #endif
 #ifndef GR_SSSP_STAGE
 #define GR_SSSP_STAGE 64
