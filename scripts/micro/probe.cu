@@ -27,7 +27,10 @@ __global__ void probe(const unsigned *bm, int iters, unsigned *sink) {
         for (int k = 0; k < 8; ++k) {
             x = hsh(x + k);
             const unsigned w = x & (kWords - 1);
-            if (MODE == 0) { unsigned r; asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(r) : "l"(bm + w)); wv[k] = r; }
+            if (MODE == 4) { wv[k] = atomicOr((unsigned *)bm + w, 1u << (x & 31)); }
+            else if (MODE == 5) { atomicOr((unsigned *)bm + w, 1u << (x & 31)); wv[k] = 0; }
+            else if (MODE == 6) { ((volatile unsigned *)bm)[w] = x; wv[k] = 0; }
+            else if (MODE == 0) { unsigned r; asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(r) : "l"(bm + w)); wv[k] = r; }
             else if (MODE == 1) wv[k] = __ldcg(bm + w);
             else if (MODE == 2) { unsigned r; asm volatile("ld.shared.u32 %0, [%1];" : "=r"(r) : "r"(sbase + 4u * (w & (half - 1)))); wv[k] = r; }
             else {
@@ -49,13 +52,15 @@ int main() {
     const int iters = 256, threads = 1024, ctas = 148;  // 1 CTA per SM
     const double probes = (double)iters * 8 * threads * ctas;
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    const char *names[] = {"L1 (ld.ca)", "L2 (ld.cg)", "smem (half bitmap)", "DSMEM cluster-2 (whole bitmap)"};
-    for (int mode = 0; mode < 4; ++mode) {
+    const char *names[] = {"L1 (ld.ca)", "L2 (ld.cg)", "smem (half bitmap)", "DSMEM cluster-2 (whole bitmap)",
+                           "atomicOr with return", "RED.OR (no return)", "plain 4-B store"};
+    for (int mode = 0; mode < 7; ++mode) {
         size_t smem = mode >= 2 ? kWords / 2 * 4 : 0;
         cudaLaunchConfig_t cfg = {}; cfg.gridDim = dim3(ctas); cfg.blockDim = dim3(threads); cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension; at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
         cfg.attrs = at; cfg.numAttrs = mode == 3 ? 1 : 0;
-        void (*k)(const unsigned *, int, unsigned *) = mode == 0 ? probe<0> : mode == 1 ? probe<1> : mode == 2 ? probe<2> : probe<3>;
+        void (*k)(const unsigned *, int, unsigned *) = mode == 0 ? probe<0> : mode == 1 ? probe<1> : mode == 2 ? probe<2>
+                                                      : mode == 3 ? probe<3> : mode == 4 ? probe<4> : mode == 5 ? probe<5> : probe<6>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(e0);
