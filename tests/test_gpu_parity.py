@@ -365,3 +365,39 @@ def test_bounded_degree_adjacency(gr, ell, cluster, monkeypatch):
     G = _dev(g, gr)
     assert G.info().bounded_degree == 0
     G.close()
+
+
+@pytest.mark.parametrize("cluster", ["1", "0"])
+def test_run_stats_bounded_degree(gr, cluster, monkeypatch):
+    """Per-level records and run totals stay exact on the bounded-degree paths:
+    levels run in the one-cluster kernel, in the grid kernel, and (the 2^18
+    tree from its root: a 32K-vertex frontier) across the cluster -> grid
+    handoff, whose records come from both kernels."""
+    monkeypatch.setenv("GR_ELL_CLUSTER", cluster)
+    for g, s in ((gg.make_config("c4_road", shrink=3), None), (gg.binary_tree(1 << 18), 0)):
+        G = _dev(g, gr)
+        assert G.info().bounded_degree == 1
+        R, C, _ = g.numpy()
+        src = gg.sources(g, 1)[0] if s is None else s
+        ref, _ = oracle.bfs(R, C, src)
+        G.bfs(src, direction="push")
+        st = G.run_stats()
+        sizes = np.bincount(ref[ref >= 0])
+        assert st["num_levels"] == len(sizes)
+        deg = np.diff(R)
+        for rec in st["levels"]:
+            L = rec["level"]
+            assert rec["frontier"] == int(((ref == L) & (deg > 0)).sum()), L
+            assert rec["frontier_edges"] == int(deg[ref == L].sum()), L
+        assert st["reached"] == int((ref >= 0).sum())
+        assert st["reached_edges"] == oracle.reached_edges(R, ref, -1)
+        gw = gg.assign_weights(g, seed=9)
+        Gw = _dev(gw, gr)
+        Rw, Cw, Ww = gw.numpy()
+        Gw.sssp(src)
+        dref, _ = oracle.sssp(Rw, Cw, Ww, src)
+        st = Gw.run_stats()
+        assert st["reached"] == int((dref != oracle.UINT32_MAX).sum())
+        assert st["reached_edges"] == oracle.reached_edges(Rw, dref, oracle.UINT32_MAX)
+        G.close()
+        Gw.close()
