@@ -77,6 +77,9 @@ struct BfsArgs {
     int64_t probe_skip_pct;    // push steps skip the culling probe while m_u >= this % of m
     int32_t lazy_r;            // grid push: row offsets of discovered vertices loaded at the flush
     int32_t bar_ns;            // GridBar backoff cap (ns)
+    int32_t pull_stay;         // direction rule: stay in pull for tiny frontiers with fewer unvisited (A-3)
+    int64_t sparse_grab;       // pull sweeps grab 32 words when u_cnt * sparse_grab < n (0: never)
+    int64_t sparse_grab_maxw;  // ... and the bitmap has at most this many words (measured: C5's 2^20 prefer 4)
     int32_t resume;            // bounded-degree graphs: the cluster kernel ran the first levels
                                // (bfs_ell_cluster_kernel); continue from ctl->bstate, no init
 };
@@ -419,7 +422,7 @@ __device__ __forceinline__ int decide_direction(const BfsArgs &a, int dir, int64
                                                 int64_t u_cnt, int64_t m_u, int64_t prev_f,
                                                 int64_t nwords) {
     return direction_rule(a.direction, a.switch_rule, a.alpha, a.beta, a.nonisolated, dir, f, mf, u_cnt, m_u,
-                          prev_f, nwords);
+                          prev_f, nwords, a.pull_stay == 2 ? INT64_MAX : a.pull_stay ? a.small_f : 0);
 }
 
 struct BfsState {  // per-traversal heuristic state, identical in every CTA
@@ -834,8 +837,11 @@ __global__ void __launch_bounds__(kBlk, kMinB) bfs_kernel(BfsArgs a) {
                 grid.sync();
             }
             PullCounts pc;
+            // few unvisited vertices left (late levels): a warp grabs 32 bitmap
+            // words at a time, so the sweep is not a chain of 4-word grabs
             pull_level(a, fb_c, fb_n, L + 1, &s->work, s->u.plist[wib], pc, sbm, snap ? sbits : 0,
-                       nwords * blockIdx.x / gridDim.x, nwords * (blockIdx.x + 1) / gridDim.x);
+                       nwords * blockIdx.x / gridDim.x, nwords * (blockIdx.x + 1) / gridDim.x,
+                       (st.u_cnt * a.sparse_grab < a.n && nwords <= a.sparse_grab_maxw) ? 32 : kPullGrab);
             ndisc = pc.ndisc;
             insp = pc.insp;
             // lazy queue: only the size, edges and max degree of the next frontier
@@ -1139,6 +1145,9 @@ gr_status run_bfs(Graph *g, int32_t src, int32_t *depth, int32_t *pred, const gr
     a.probe_skip_pct = env_int("GR_PROBE_SKIP_PCT", 75);
     a.lazy_r = (int32_t)env_int("GR_LAZY_R", 1);
     a.bar_ns = (int32_t)env_int("GR_BAR_NS", 128);
+    a.pull_stay = (int32_t)env_int("GR_PULL_STAY", 2);
+    a.sparse_grab = env_int("GR_SPARSE_GRAB", 16);
+    a.sparse_grab_maxw = env_int("GR_SPARSE_GRAB_MAXW", 1 << 18);
     if (a.small_f > kSmallF) a.small_f = kSmallF;
 
     // Kernel variant: graphs whose bitmap no

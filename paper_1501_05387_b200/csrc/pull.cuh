@@ -64,7 +64,7 @@ template <class A>
 __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restrict__ fcur,
                                            uint32_t *__restrict__ fnext, int32_t next_depth, int *swork,
                                            int32_t *wl, PullCounts &pc, uint32_t sbm, int64_t sbits,
-                                           int64_t wb0, int64_t wb1) {
+                                           int64_t wb0, int64_t wb1, int grab = kPullGrab) {
     const int64_t nwords = (a.n + 31) / 32;
     const unsigned l = lane_id();
     const unsigned long long pol = policy_evict_first();
@@ -251,12 +251,12 @@ __device__ __forceinline__ void pull_level(const A &a, const uint32_t *__restric
     };
     for (;;) {
         int c = 0;
-        if (l == 0) c = atomicAdd(swork, kPullGrab);
+        if (l == 0) c = atomicAdd(swork, grab);
         c = __shfl_sync(0xffffffffu, c, 0);
         const int64_t w0 = wb0 + c;
         if (w0 >= wb1) break;
         const int64_t wi = w0 + l;
-        uint32_t cm = ((int)l < kPullGrab && wi < wb1) ? ~a.visited[wi] : 0u;
+        uint32_t cm = ((int)l < grab && wi < wb1) ? ~a.visited[wi] : 0u;
         if (wi == nwords - 1) cm &= tail;
         // word by word, lane b takes bit b: the list stays sorted by vertex id,
         // so a batch's depth/pred stores and bitmap REDs touch few lines
@@ -311,14 +311,20 @@ __device__ __forceinline__ void bitmap_to_queue(const A &a, const uint32_t *__re
 //   dir          direction of the previous step (1 push, 2 pull)
 __device__ __forceinline__ int direction_rule(int forced, int switch_rule, double alpha, double beta,
                                               int64_t nonisolated, int dir, int64_t f, int64_t mf,
-                                              int64_t u_cnt, int64_t m_u, int64_t prev_f, int64_t nwords) {
+                                              int64_t u_cnt, int64_t m_u, int64_t prev_f, int64_t nwords,
+                                              int64_t stay_f = 0) {
     if (forced != 0) return forced;
     if (switch_rule == 1) return (u_cnt < f) ? 2 : 1;
     if (dir == 1) {
         if ((double)mf > (double)m_u / alpha && mf >= nwords) return 2;
         return 1;
     }
-    if ((double)f < (double)nonisolated / beta && f < prev_f) return 1;
+    // ... unless fewer vertices are left unvisited than the frontier holds
+    // (the literal rule's pull condition) and the frontier is at most stay_f:
+    // one more pull step then touches fewer vertices than the push step and
+    // saves the bitmap -> queue conversion (measured: stay_f
+    // unlimited in bfs.cu, 0 -- plain Beamer -- in the partitioned kernel)
+    if ((double)f < (double)nonisolated / beta && f < prev_f && !(f <= stay_f && u_cnt < f)) return 1;
     return 2;
 }
 
