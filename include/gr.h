@@ -140,7 +140,7 @@ typedef struct {
                             culling heuristics (A-5, A-6)    */
     int32_t switch_rule; /* 0 Beamer alpha/beta (default), 1 paper-literal
                             "unvisited < frontier" (A-3)                */
-    double alpha, beta;  /* Beamer parameters; 0 = 14, 24                          */
+    double alpha, beta;  /* Beamer parameters; 0 = 20, 24 (single GPU; 14, 24 partitioned) */
     int64_t lb_threshold;/* frontier size at which auto strategy switches from
                             node-granular to edge-granular balancing; 0 = default
                             65536 (swept on B200, scripts/lb_sweep.py; auto also
