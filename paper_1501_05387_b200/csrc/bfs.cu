@@ -29,7 +29,7 @@ namespace gr {
 #endif
 constexpr int64_t kSmallF = GR_SMALL_CAP;  // small mode: queue capacity (shared memory)
 constexpr int64_t kSmallFDefault = 512;   // small mode: default max frontier (swept on C4)
-constexpr int64_t kSmallE = 16384;  // small mode: max frontier edges
+constexpr int64_t kSmallE = 4096;   // small mode: max frontier edges (swept round 2: 4096 / 16384 / 65536: C1 0.079 / 0.086 / 0.086 ms, C2-C5 equal or better at 4096)
 #ifndef GR_BFS_STAGES
 #define GR_BFS_STAGES 0  // measured on C2 push: 2 and 4 stages are slower (smem displaces L1)
 #endif
