@@ -587,7 +587,7 @@ static gr_status launch_pbfs(Graph **gs, int k, int64_t src, int32_t **depth, in
     A.inbox_cap = Ly.inbox_cap;
     A.direction = o.direction;
     A.switch_rule = o.switch_rule;
-    A.alpha = o.alpha > 0 ? o.alpha : 14.0;
+    A.alpha = o.alpha > 0 ? o.alpha : (double)env_int("GR_PALPHA", 14);
     A.beta = o.beta > 0 ? o.beta : 24.0;
     A.lb_chunks = (int32_t)env_int("GR_LB_CHUNKS", 4);
     const void *fn = (const void *)pbfs_kernel<kPBlock, kPMinB>;
