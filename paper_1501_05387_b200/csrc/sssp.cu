@@ -27,6 +27,7 @@ struct SsspArgs {
     int32_t bar_ns;           // GridBar backoff cap (ns)
     int32_t resume;           // bounded-degree graphs: sssp_ell_cluster_kernel ran the first steps
     int32_t cl_stamp;         // cluster near iterations dedupe appends by stamp (1) or not (0)
+    int32_t cl_farres;        // cluster near iterations reserve far slots before the atomicMin (1)
     uint32_t *fb;             // pull steps: bitmap of the near frontier [ceil(n/32)]
     int32_t direction;        // 0 auto, 1 push, 2 pull (near iterations; reading A-24)
     double alpha;             // auto: pull when m_f * alpha > m
@@ -452,6 +453,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
             unsigned long long mymin = ~0ull;
             for (int64_t j = tid; j < fc; j += nthreads) {
                 const int32_t v = far_c[j];
+                if (v < 0) continue;  // sentinel of the cluster kernel's reserved far slots
                 const unsigned long long d = ld_probe(a.dp + v, pol_keep) >> 32;
                 if (d >= thr && d < mymin) mymin = d;
             }
@@ -483,7 +485,7 @@ __global__ void __launch_bounds__(kBlock, kMinBlocks) sssp_kernel(SsspArgs a) {
                 bool to_near = false, to_far = false;
                 int32_t v = 0;
                 int64_t deg = 0, rs = 0;
-                if (j < fc) {
+                if (j < fc && far_c[j] >= 0) {
                     v = far_c[j];
                     const unsigned long long d = ld_probe(a.dp + v, pol_keep) >> 32;
                     const int64_t r0 = nearq.Rl ? 0 : a.R[v], r1 = nearq.Rl ? 0 : a.R[v + 1];  // with d
@@ -679,10 +681,22 @@ __global__ void __launch_bounds__(kClBlock, 1) sssp_ell_cluster_kernel(SsspArgs 
             const int32_t wt[4] = {wt4.x, wt4.y, wt4.z, wt4.w};
             unsigned long long nd[4], old[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                nd[q] = du + (unsigned long long)((uint32_t)wt[q] >> 3);
-                old[q] = id[q] >= 0 ? atomicMin(a.dp + id[q], (nd[q] << 32) | 0xffffffffull) : 0ull;
+            for (int q = 0; q < 4; ++q) nd[q] = du + (unsigned long long)((uint32_t)wt[q] >> 3);
+            // far-pile slots for every relaxation that WOULD go far, reserved now
+            // (one atomic per warp, in flight with the atomicMins below); slots of
+            // relaxations that do not improve get the sentinel -1, which the
+            // re-splits skip -- the far append costs no round trip of its own
+            int npf = 0;
+            if (a.cl_farres) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) npf += (id[q] >= 0 && nd[q] >= thr);
             }
+            const int pfi = warp_incl_scan<int>(npf);
+            unsigned long long fbase = 0;
+            if (l == 31 && pfi > 0) fbase = atomicAdd(&a.ctl->far_count[fp], (unsigned long long)pfi);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                old[q] = id[q] >= 0 ? atomicMin(a.dp + id[q], (nd[q] << 32) | 0xffffffffull) : 0ull;
             bool imp[4], far[4];
             int32_t ex[4];
             const int32_t key_base = 2 * it;
@@ -713,15 +727,30 @@ __global__ void __launch_bounds__(kClBlock, 1) sssp_ell_cluster_kernel(SsspArgs 
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(a.dp + id[q]));
                 }
             }
+            if (a.cl_farres) {
+                fbase = __shfl_sync(0xffffffffu, fbase, 31);
+                int64_t pos = (int64_t)fbase + pfi - npf;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                cl_far_push(tofar[q], id[q], a.far[fp], &a.ctl->far_count[fp], a.far_cap, &a.ctl->overflow);
+                for (int q = 0; q < 4; ++q) {
+                    if (id[q] >= 0 && nd[q] >= thr) {
+                        if (pos < a.far_cap) a.far[fp][pos] = tofar[q] ? id[q] : -1;
+                        else atomicExch(&a.ctl->overflow, 2ull);
+                        ++pos;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    cl_far_push(tofar[q], id[q], a.far[fp], &a.ctl->far_count[fp], a.far_cap, &a.ctl->overflow);
+            }
         } else {
             // ---- far re-split (A-11): minimum live far distance, then split --
             const int32_t *far_c = a.far[fp];
             unsigned long long mymin = ~0ull;
             for (int64_t j = (int64_t)t * K + rank; j < fc; j += (int64_t)K * kClBlock) {
-                const unsigned long long d = ld_probe(a.dp + far_c[j], pol) >> 32;
+                const int32_t v = far_c[j];
+                if (v < 0) continue;  // reserved slot of a relaxation that did not improve
+                const unsigned long long d = ld_probe(a.dp + v, pol) >> 32;
                 if (d >= thr && d < mymin) mymin = d;
             }
 #pragma unroll
@@ -757,7 +786,7 @@ __global__ void __launch_bounds__(kClBlock, 1) sssp_ell_cluster_kernel(SsspArgs 
                     bool tonear = false, tofar = false;
                     int32_t v = 0;
                     int64_t deg = 0;
-                    if (j < fc) {
+                    if (j < fc && far_c[j] >= 0) {
                         v = far_c[j];
                         const unsigned long long d = ld_probe(a.dp + v, pol) >> 32;
                         const int64_t r0 = a.R[v], r1 = a.R[v + 1];
@@ -846,6 +875,7 @@ gr_status run_sssp(Graph *g, int32_t src, uint32_t *dist, int32_t *pred, uint64_
     a.lazy_r = (int32_t)env_int("GR_LAZY_R", 1);
     a.bar_ns = (int32_t)env_int("GR_BAR_NS", 128);
     a.cl_stamp = (int32_t)env_int("GR_CL_STAMP", 0);  // measured: C4 SSSP 104 -> 94 ms without
+    a.cl_farres = (int32_t)env_int("GR_CL_FARRES", 1);
     a.direction = direction;
     a.alpha = alpha > 0 ? alpha : 2.0;  // measured on C3: pull pays only when m_f > m / 2
     a.dp = g->dp; a.stamp = g->stamp;
